@@ -1,0 +1,176 @@
+/*
+ * infinigen_b200.h -- C ABI of the B200 decode-time KV path (InfiniGen,
+ * arXiv 2406.19707).  Plain C types only; every call enqueues on the caller's
+ * CUDA stream (passed as void*), never synchronises the host, never allocates
+ * device memory, and returns an int status (IG_OK == 0).
+ *
+ * The reference exposes this path as Python operators that its engine imports
+ * by name (reference: pkg/src/speckv/engine.py:27-38).  Each entry point below
+ * names the reference interface it replaces; the Python shims in
+ * paper_2406_19707_b200/ keep the reference signatures and map statuses back
+ * to the reference exception classes (ValueError / IndexError /
+ * ArtifactConsistencyError).
+ *
+ * Layouts (row-major, all per layer unless noted; Hg = heads on this GPU):
+ *   host pool   T[B][Hg][S_max][2][d]      K row then V row, T = f32|f16|bf16
+ *   partial K   f32[B][Hg][k][S_max]       column-major over tokens (coalesced)
+ *   cols        i32[B][Hg][k]              ascending skewed-column indices
+ *   scores      f32[B][Hg][S_max]
+ *   idx         i32[B][Hg][cap]            selected rows, ascending
+ *   stage       T[B][Hg][cap][2][d]        fetched rows in HBM
+ *   pool meta   i64 arrival[B][Hg][S_max], i64 last_fetch[...], u8 counter[...]
+ */
+#ifndef INFINIGEN_B200_H
+#define INFINIGEN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  IG_OK = 0,
+  IG_EINVAL = 1,        /* bad shape/argument  -> ValueError (speculation.py:51-54, 124-132) */
+  IG_ERANGE = 2,        /* index out of range  -> IndexError (pool.py:91-92)                  */
+  IG_ECONSISTENCY = 3,  /* pool / partial-K desync -> ArtifactConsistencyError (speculation.py:107-114) */
+  IG_ENOMEM = 4,
+  IG_ECUDA = 1000       /* IG_ECUDA + cudaError_t */
+};
+
+enum { IG_ELT_F32 = 0, IG_ELT_F16 = 1, IG_ELT_BF16 = 2 };
+/* EvictionPolicy (pool.py:22-25) */
+enum { IG_POLICY_FIFO = 0, IG_POLICY_LRU = 1, IG_POLICY_COUNTER = 2 };
+
+/* Per-session decode position, resident in device memory so a whole decode
+ * step can be enqueued (or graph-captured) without host round trips.
+ *   s_len : pool rows before this step's append (len(pool), engine.py:329)
+ *   limit : pool_limit, 0 = unlimited (engine.py:58, pool.py:61)
+ *   seq   : KvPool._seq of every pool (pool.py:50-51); each decode step does
+ *           one append (+1) and one fetch (+1) on every pool.             */
+typedef struct ig_step_state {
+  int32_t s_len;
+  int32_t limit;
+  int64_t seq;
+  int32_t step;
+  int32_t reserved;
+} ig_step_state;
+
+int ig_abi_version(void);
+const char* ig_status_string(int status);
+
+/* ---- host KV pool storage: replaces KvPool.keys/values (pool.py:37-38) ---- */
+/* Pinned, mapped, portable host allocation; *dev_ptr is its device alias.   */
+int ig_host_alloc(size_t bytes, void** host_ptr, void** dev_ptr);
+int ig_host_free(void* host_ptr);
+
+/* ---- K1 rehearsal: replaces speculate_scores (speculation.py:117-135) -----
+ * qspec = x_a(prev layer) @ W_Q(layer)[:, local heads] (f32[B][ldq]).  Per
+ * (b, h): score[t] = (sum_j qspec[b, h*d + cols[j]] * pk[j][t]) * scale for
+ * t < st->s_len, and maxkey[b,h] = max over t (order-preserving u32 key,
+ * atomically max-reduced, so maxkey must be zeroed before the call).        */
+int ig_rehearse(const float* qspec, int ldq, const int32_t* cols, const float* pk,
+                const ig_step_state* st, int B, int Hg, int d, int k, int S_max,
+                float scale, float* scores, uint32_t* maxkey, void* stream);
+
+/* Row maxima (as order keys) of scores not produced by ig_rehearse (the
+ * select_tokens shim, speculation.py:156).                                  */
+int ig_score_max(const float* scores, const ig_step_state* st, int B, int Hg, int S_max,
+                 uint32_t* maxkey, void* stream);
+
+/* ---- K2a count: select_tokens lines speculation.py:154-157 ---------------
+ * counts[b,h] = #{t < s : score[t] > float32(double(max) - alpha)};
+ * count_sum[b] += sum_h counts[b,h] (atomic; zero it first).               */
+int ig_count(const float* scores, const uint32_t* maxkey, const ig_step_state* st,
+             int B, int Hg, int S_max, double alpha, int32_t* counts,
+             int32_t* count_sum, void* stream);
+
+/* ---- K2b select: speculation.py:158-163 + topk_indices linalg.py:177-185 --
+ * n[b] = min(clamp(floor(count_sum[b]/H_total + 0.5), min_select, cap), s),
+ * cap = max(floor(cap_ratio*s), min_select); idx[b,h,0:n] = the top-n rows of
+ * score[b,h] (ties -> lower index), written in ASCENDING row order.
+ * Fails with IG_EINVAL at run time if n would exceed cap_max (buffer size). */
+int ig_select(const float* scores, const int32_t* count_sum, const ig_step_state* st,
+              int B, int Hg, int H_total, int S_max, int cap_max, double cap_ratio,
+              int min_select, int32_t* idx, int32_t* n_out, int32_t* err_flag,
+              void* stream);
+
+/* Drop-in ordering: rewrite idx[b,h,0:n] in the reference's stable
+ * descending-score order (linalg.py:184).  Used by the select_tokens shim,
+ * not by the engine (the engine fetches in ascending order).              */
+int ig_order_by_score(const float* scores, const int32_t* n, int B, int Hg,
+                      int S_max, int cap, int32_t* idx, void* stream);
+
+/* Generic top-k per row (ties -> lower index), ascending output.  Used for
+ * build_partial's column choice (speculation.py:41-58).                   */
+int ig_topk_rows(const float* values, int rows, int len, int k, int32_t* idx_out,
+                 void* stream);
+
+/* ---- K3 fetch: replaces KvPool.fetch's gather (pool.py:83-99) ------------
+ * Zero-copy SM gather of the selected rows from the mapped host pool into
+ * stage.  pool_dev = device alias of this layer's T[B][Hg][S_max][2][d].   */
+int ig_fetch(const void* pool_dev, const int32_t* idx, const int32_t* n, int B, int Hg,
+             int S_max, int cap, int row_bytes, void* stage, int ctas, void* stream);
+/* Layer 0 (engine.py:393-396): every row [0, s) by copy engine, host sizes. */
+int ig_fetch_all(const void* pool_host, int B, int Hg, int S_max, int s, int row_bytes,
+                 void* stage, int stage_rows, void* stream);
+
+/* ---- K5 append: KvPool.append (pool.py:53-81) + evict_select (:101-109) +
+ * append_partial_key (speculation.py:92-114) + the fetch-metadata update of
+ * KvPool.fetch (pool.py:93-98) for this layer's fetch set.
+ * Per (b, h): pos = s (below limit) or the policy victim; the new K/V row is
+ * stored to the host pool, k_cur[cols] into pk[:, pos], metadata reset to
+ * seq+1; then (fetch_mode 1) every row, or (fetch_mode 2) the selection
+ * idx[0:n] plus pos deduplicated (engine.py:449-453), gets last_fetch = seq+2
+ * and a saturating counter bump with "any counter hit 255 -> halve all";
+ * fetch_mode 0 is a plain KvPool.append.  pos_out[b,h] receives pos;
+ * events[b,h] = {victim, old arrival} on overwrite else {-1, 0}.            */
+int ig_append(const float* k_cur, const float* v_cur, int ldkv, void* pool_dev, int elt,
+              float* pk, const int32_t* cols, int k, int64_t* arrival, int64_t* last_fetch,
+              uint8_t* counter, int policy, int fetch_mode, const int32_t* idx,
+              const int32_t* n, int cap, const ig_step_state* st, int B, int Hg, int d,
+              int S_max, int32_t* pos_out, int64_t* events, void* stream);
+
+/* KvPool.evict_select (pool.py:101-109) alone: victim[b,h] = argmin over
+ * [0, st->s_len) of the policy key, lowest index on ties.                  */
+int ig_evict_select(const int64_t* arrival, const int64_t* last_fetch, const uint8_t* counter,
+                    int policy, const ig_step_state* st, int B, int Hg, int S_max,
+                    int32_t* victim, void* stream);
+
+/* KvPool.fetch metadata alone (pool.py:93-98): rows idx[b,h,0:n[b]] (unique)
+ * get last_fetch = seq and a saturating counter bump; halve-all over
+ * [0, st->s_len) if any reaches 255.                                       */
+int ig_touch(const int32_t* idx, const int32_t* n, int cap, const ig_step_state* st, int B,
+             int Hg, int S_max, int64_t seq, int64_t* last_fetch, uint8_t* counter,
+             void* stream);
+
+/* ---- K4 attend: replaces attention_head on the fetched set (model.py:156-180,
+ * engine.py:352-358).  Per (b, h): softmax((q . K^T) / float32(sqrt(d))) . V
+ * over stage rows r < n (n == NULL -> s rows, idx == NULL -> row r) whose row
+ * index != pos, plus the GPU-resident current row (k_cur, v_cur).  Split
+ * over row chunks; partial/ticket are scratch sized by ig_attend_scratch.   */
+int ig_attend_scratch(int B, int Hg, int d, int cap, size_t* partial_floats,
+                      size_t* tickets);
+int ig_attend(const float* q, int ldq, const float* k_cur, const float* v_cur, int ldkv,
+              const void* stage, int elt, const int32_t* idx, const int32_t* n,
+              const int32_t* pos, const ig_step_state* st, int B, int Hg, int d, int cap,
+              float* partial, int32_t* tickets, float* out, int ldo, void* stream);
+
+/* Strided 2-D copy between any UVA addresses (cudaMemcpyDefault): used to
+ * write prefill K/V rows into the host pool (engine.py:265-266).          */
+int ig_memcpy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                size_t height, void* stream);
+
+/* ---- step bookkeeping -------------------------------------------------- */
+/* s_len = min(s_len + 1, limit), seq += 2, step += 1 (engine.py:377-378). */
+int ig_step_advance(ig_step_state* st, void* stream);
+
+/* Reference layernorm (linalg.py:50-69): (x-mean)/sqrt(var+eps)*g+b, f32. */
+int ig_layernorm(const float* x, const float* gain, const float* bias, float eps,
+                 int rows, int D, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INFINIGEN_B200_H */

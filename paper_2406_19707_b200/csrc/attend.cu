@@ -1,0 +1,235 @@
+// K4 sparse decode attention over the fetched rows plus the GPU-resident
+// current row (reference attention_head model.py:156-180 as called at
+// engine.py:352-358 on the fetch set of engine.py:382-418).
+//
+// Split-KV: CTA (chunk, h, b) streams kAttChunk staged rows; each warp keeps an
+// online softmax over its rows; the CTA writes (m, l, acc[d]) and the last CTA
+// of a (b, h) to arrive (ticket) merges the chunks in fixed chunk order, so the
+// result is deterministic.  Scores are (q . k) / float32(sqrt(d)) -- a division,
+// as in model.py:174 -- and exp is the full-precision expf.
+#include "common.cuh"
+
+namespace ig {
+
+constexpr int kAttThreads = 128;
+constexpr int kAttWarps = kAttThreads / kWarp;
+constexpr int kAttChunk = 128;     // staged rows per CTA
+constexpr int kAttMaxPer = 8;      // head_dim <= 256
+constexpr int kAttRowsInFlight = 4;
+
+// Lane l owns elements l*E .. l*E+E-1 when E > 0 (d == 32*E, vector loads);
+// for other head dims (E == 0) lane l owns l, l+32, ... (scalar loads).
+template <typename T, int E>
+struct RowIO {
+  static constexpr int kPer = E > 0 ? E : kAttMaxPer;
+  __device__ static int elem(int lane, int j) { return E > 0 ? lane * E + j : lane + 32 * j; }
+  __device__ static void load(const T* row, int lane, int d, float* out) {
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int e = elem(lane, j);
+      out[j] = e < d ? Elt<T>::to_f(row[e]) : 0.f;
+    }
+  }
+};
+
+template <typename T, int E>
+__global__ void __launch_bounds__(kAttThreads)
+attend_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_cur,
+              const float* __restrict__ v_cur, int ldkv, const T* __restrict__ stage,
+              const int32_t* __restrict__ idx, const int32_t* __restrict__ n_in,
+              const int32_t* __restrict__ pos_in, const ig_step_state* __restrict__ st, int Hg,
+              int d, int cap, float inv_dummy, float sqrt_d, int max_chunks,
+              float* __restrict__ partial, int32_t* __restrict__ tickets, float* __restrict__ out,
+              int ldo) {
+  using IO = RowIO<T, E>;
+  constexpr int P = IO::kPer;
+  const int b = blockIdx.z, h = blockIdx.y, c = blockIdx.x;
+  const size_t bh = (size_t)b * Hg + h;
+  const int rows = n_in ? n_in[b] : st->s_len;
+  const int nchunks = max(1, (rows + kAttChunk - 1) / kAttChunk);
+  if (c >= nchunks) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int pos = pos_in[bh];
+
+  float qv[P];
+  {
+    const float* qr = q + (size_t)b * ldq + (size_t)h * d;
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int e = IO::elem(lane, j);
+      qv[j] = e < d ? qr[e] : 0.f;
+    }
+  }
+  float m = -INFINITY, l = 0.f, acc[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) acc[j] = 0.f;
+
+  auto consume = [&](float sc, const float* vv) {
+    const float mn = fmaxf(m, sc);
+    const float corr = expf(m - mn);  // m == -inf -> 0
+    const float p = expf(sc - mn);
+    l = l * corr + p;
+#pragma unroll
+    for (int j = 0; j < P; ++j) acc[j] = fmaf(p, vv[j], acc[j] * corr);
+    m = mn;
+  };
+
+  const int r0 = c * kAttChunk, r1 = min(rows, r0 + kAttChunk);
+  const T* base = stage + bh * (size_t)cap * 2 * d;
+  for (int rb = r0 + w * kAttRowsInFlight; rb < r1; rb += kAttWarps * kAttRowsInFlight) {
+    float kk[kAttRowsInFlight][P], vv[kAttRowsInFlight][P];
+    bool ok[kAttRowsInFlight];
+#pragma unroll
+    for (int u = 0; u < kAttRowsInFlight; ++u) {
+      const int r = rb + u;
+      ok[u] = r < r1 && (idx ? idx[bh * cap + r] : r) != pos;
+      if (ok[u]) {
+        IO::load(base + (size_t)r * 2 * d, lane, d, kk[u]);
+        IO::load(base + (size_t)r * 2 * d + d, lane, d, vv[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kAttRowsInFlight; ++u) {
+      if (!ok[u]) continue;  // warp-uniform
+      float dot = 0.f;
+#pragma unroll
+      for (int j = 0; j < P; ++j) dot = fmaf(qv[j], kk[u][j], dot);
+      dot = warp_sum(dot);
+      consume(dot / sqrt_d, vv[u]);
+    }
+  }
+  if (c == 0 && w == 0) {  // the current token: GPU-resident, never fetched
+    const float* kr = k_cur + (size_t)b * ldkv + (size_t)h * d;
+    const float* vr = v_cur + (size_t)b * ldkv + (size_t)h * d;
+    float kk[P], vv[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+      const int e = IO::elem(lane, j);
+      kk[j] = e < d ? kr[e] : 0.f;
+      vv[j] = e < d ? vr[e] : 0.f;
+    }
+    float dot = 0.f;
+#pragma unroll
+    for (int j = 0; j < P; ++j) dot = fmaf(qv[j], kk[j], dot);
+    dot = warp_sum(dot);
+    consume(dot / sqrt_d, vv);
+  }
+
+  // merge the warps of this CTA (fixed order)
+  __shared__ float wm[kAttWarps], wl[kAttWarps];
+  __shared__ float wacc[kAttWarps][kAttMaxPer * 32];
+  if (lane == 0) { wm[w] = m; wl[w] = l; }
+#pragma unroll
+  for (int j = 0; j < P; ++j) {
+    const int e = IO::elem(lane, j);
+    if (e < d) wacc[w][e] = acc[j];
+  }
+  __syncthreads();
+  float* part = partial + (bh * max_chunks + c) * (size_t)(d + 2);
+  if (threadIdx.x == 0) {
+    float M = -INFINITY;
+    for (int i = 0; i < kAttWarps; ++i) M = fmaxf(M, wm[i]);
+    float L = 0.f;
+    for (int i = 0; i < kAttWarps; ++i) L += wl[i] * (wm[i] == -INFINITY ? 0.f : expf(wm[i] - M));
+    part[0] = M;
+    part[1] = L;
+  }
+  {
+    float M = -INFINITY;
+    for (int i = 0; i < kAttWarps; ++i) M = fmaxf(M, wm[i]);
+    for (int e = threadIdx.x; e < d; e += blockDim.x) {
+      float a = 0.f;
+      for (int i = 0; i < kAttWarps; ++i)
+        a += wacc[i][e] * (wm[i] == -INFINITY ? 0.f : expf(wm[i] - M));
+      part[2 + e] = a;
+    }
+  }
+  // last CTA of this (b, h) merges all chunks
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(tickets + bh, 1) == nchunks - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const float* pb = partial + bh * max_chunks * (size_t)(d + 2);
+  float M = -INFINITY;
+  for (int i = 0; i < nchunks; ++i) M = fmaxf(M, __ldcg(pb + (size_t)i * (d + 2)));
+  float L = 0.f;
+  for (int i = 0; i < nchunks; ++i) {
+    const float mi = __ldcg(pb + (size_t)i * (d + 2));
+    L += __ldcg(pb + (size_t)i * (d + 2) + 1) * (mi == -INFINITY ? 0.f : expf(mi - M));
+  }
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    float a = 0.f;
+    for (int i = 0; i < nchunks; ++i) {
+      const float mi = __ldcg(pb + (size_t)i * (d + 2));
+      a += __ldcg(pb + (size_t)i * (d + 2) + 2 + e) * (mi == -INFINITY ? 0.f : expf(mi - M));
+    }
+    out[(size_t)b * ldo + (size_t)h * d + e] = a / L;
+  }
+  if (threadIdx.x == 0) tickets[bh] = 0;
+}
+
+template <typename T>
+int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const float* k_cur,
+                  const float* v_cur, int ldkv, const void* stage, const int32_t* idx,
+                  const int32_t* n, const int32_t* pos, const ig_step_state* st, int Hg, int d,
+                  int cap, float sqrt_d, int max_chunks, float* partial, int32_t* tickets,
+                  float* out, int ldo) {
+#define IG_ATT(E)                                                                              \
+  attend_kernel<T, E><<<grid, kAttThreads, 0, s>>>(q, ldq, k_cur, v_cur, ldkv,                \
+      (const T*)stage, idx, n, pos, st, Hg, d, cap, 0.f, sqrt_d, max_chunks, partial, tickets, \
+      out, ldo)
+  switch (d) {
+    case 32: IG_ATT(1); break;
+    case 64: IG_ATT(2); break;
+    case 128: IG_ATT(4); break;
+    case 256: IG_ATT(8); break;
+    default: IG_ATT(0); break;
+  }
+#undef IG_ATT
+  IG_LAUNCH_STATUS();
+  return IG_OK;
+}
+
+}  // namespace ig
+
+extern "C" int ig_attend_scratch(int B, int Hg, int d, int cap, size_t* partial_floats,
+                                 size_t* tickets) {
+  using namespace ig;
+  if (B < 1 || Hg < 1 || d < 1 || cap < 1 || !partial_floats || !tickets) return IG_EINVAL;
+  const int max_chunks = (cap + kAttChunk - 1) / kAttChunk;
+  *partial_floats = (size_t)B * Hg * max_chunks * (d + 2);
+  *tickets = (size_t)B * Hg;
+  return IG_OK;
+}
+
+extern "C" int ig_attend(const float* q, int ldq, const float* k_cur, const float* v_cur, int ldkv,
+                         const void* stage, int elt, const int32_t* idx, const int32_t* n,
+                         const int32_t* pos, const ig_step_state* st, int B, int Hg, int d, int cap,
+                         float* partial, int32_t* tickets, float* out, int ldo, void* stream) {
+  using namespace ig;
+  if (!q || !k_cur || !v_cur || !stage || !pos || !st || !partial || !tickets || !out || B < 1 ||
+      Hg < 1 || d < 1 || d > 32 * kAttMaxPer || cap < 1 || ldq < Hg * d || ldkv < Hg * d ||
+      ldo < Hg * d)
+    return IG_EINVAL;
+  const int max_chunks = (cap + kAttChunk - 1) / kAttChunk;
+  dim3 grid(max_chunks, Hg, B);
+  const float sqrt_d = (float)sqrt((double)d);  // float32(np.sqrt(d)), model.py:174
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (elt) {
+    case IG_ELT_F32:
+      return launch_attend<float>(grid, s, q, ldq, k_cur, v_cur, ldkv, stage, idx, n, pos, st, Hg,
+                                  d, cap, sqrt_d, max_chunks, partial, tickets, out, ldo);
+    case IG_ELT_F16:
+      return launch_attend<__half>(grid, s, q, ldq, k_cur, v_cur, ldkv, stage, idx, n, pos, st,
+                                   Hg, d, cap, sqrt_d, max_chunks, partial, tickets, out, ldo);
+    case IG_ELT_BF16:
+      return launch_attend<__nv_bfloat16>(grid, s, q, ldq, k_cur, v_cur, ldkv, stage, idx, n, pos,
+                                          st, Hg, d, cap, sqrt_d, max_chunks, partial, tickets,
+                                          out, ldo);
+    default:
+      return IG_EINVAL;
+  }
+}

@@ -1,0 +1,629 @@
+"""B200 decode engine: the batched, stream-overlapped InfiniGen decode path.
+
+Mirrors the reference inference controller (engine.py:199-477): the same
+RunConfig fields, the same per-layer order as DecodeSession.decode_step
+(engine.py:309-375), and a schema-v1 Trace (engine.py:83-196).  Differences
+are in HOW, not WHAT:
+
+  * all B sequences advance together (the reference loops over them,
+    engine.py:468-476); every hot op is one launch over (b, h);
+  * the KV pool is one pinned host allocation T[L][B][Hg][S_max][2][d]
+    (fp16 by default: the reference's 2-byte accounting, engine.py:63) and
+    its metadata lives in HBM;
+  * two CUDA streams: the compute stream runs LN / rehearsal / selection /
+    QKV / append / attention / W_O / FFN; the fetch stream moves the rows
+    layer i needs from the host pool while layer i-1 computes (the overlap
+    the reference models analytically in costmodel.py:102-139);
+  * with tensor parallelism over heads, each rank owns H/G heads, their
+    pools and partial keys; per layer it all-reduces the B head-count sums
+    (n averages over ALL heads, speculation.py:154-158) and the W_O output.
+
+Hot ops are the library kernels (ig_rehearse, ig_count, ig_select, ig_fetch,
+ig_fetch_all, ig_append, ig_attend, ig_layernorm); the dense projections
+are plain fp32 cuBLAS GEMMs with TF32 off.  No CPU fallback exists.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .prefill import causal_attention, layernorm, partial_columns
+from .speculation import SpeculationConfig, selection_bytes
+from .pool import EvictionPolicy
+
+TRACE_SCHEMA_VERSION = 1
+_TORCH_ELT = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}
+
+
+@dataclass(frozen=True)
+class RunConfig:
+    """Reference RunConfig (engine.py:51-80) for the schemes on the path."""
+    scheme: str = "speculative"            # "speculative" | "full"
+    prompt_len: int = 32
+    gen_len: int = 8
+    batch: int = 1
+    speculation: SpeculationConfig = field(default_factory=SpeculationConfig)
+    pool_limit: int | None = None
+    pool_policy: EvictionPolicy = EvictionPolicy.COUNTER
+    prompt_seed: int = 0
+    kv_bytes_per_element: int = 2
+    record_scores: bool = False
+    record_selection: bool = False
+
+    def validate(self) -> None:
+        if getattr(self.scheme, "value", self.scheme) not in ("speculative", "full"):
+            raise ValueError(f"scheme {self.scheme!r} is not on the B200 path")
+        if self.prompt_len < 1:
+            raise ValueError("prompt_len must be >= 1")
+        if self.gen_len < 0:
+            raise ValueError("gen_len must be >= 0")
+        if self.batch < 1:
+            raise ValueError("batch must be >= 1")
+        self.speculation.validate()
+        if self.pool_limit is not None and self.pool_limit < 1:
+            raise ValueError("pool_limit must be >= 1 when set")
+
+
+def _f32(a, device):
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=torch.float32).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(device)
+
+
+def _enable_ieee_fp32():
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    try:
+        torch.backends.cuda.matmul.fp32_precision = "ieee"
+    except (AttributeError, RuntimeError):
+        pass
+
+
+class HostPool:
+    """Pinned, mapped, portable host memory for the KV rows (ig_host_alloc)."""
+
+    def __init__(self, nbytes: int):
+        host, dev = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.call("ig_host_alloc", nbytes, ctypes.byref(host), ctypes.byref(dev), kernels=0)
+        self.host, self.dev, self.nbytes = host.value, dev.value, nbytes
+
+    def numpy(self, dtype, shape) -> np.ndarray:
+        """Host view (no copy) -- inspection and tests."""
+        buf = (ctypes.c_uint8 * self.nbytes).from_address(self.host)
+        return np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+    def close(self) -> None:
+        if self.host:
+            _lib.call("ig_host_free", self.host, kernels=0)
+            self.host = self.dev = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _simulate_prefill_rows(n: int, limit: int | None, policy: EvictionPolicy):
+    """Row of each prompt token and the resulting metadata when N prompt rows
+    are appended to an empty pool (engine.py:265-266 -> pool.py:53-81).  All
+    pools see the same appends and no fetches during prefill, so one
+    simulation serves every (layer, head, sequence)."""
+    rows = min(n, limit) if limit else n
+    arrival = np.zeros(rows, np.int64)
+    lastf = np.zeros(rows, np.int64)
+    ctr = np.zeros(rows, np.uint8)
+    row_of = np.empty(n, np.int64)
+    overwrites = 0
+    for t in range(n):
+        seq = t + 1
+        if limit is None or t < limit:
+            r = t
+        else:
+            key = {EvictionPolicy.FIFO: arrival, EvictionPolicy.LRU: lastf,
+                   EvictionPolicy.COUNTER: ctr}[EvictionPolicy(policy)]
+            r = int(np.argmin(key))
+            overwrites += 1
+        row_of[t] = r
+        arrival[r] = lastf[r] = seq
+        ctr[r] = 0
+    return row_of, arrival, lastf, ctr, overwrites
+
+
+class DecodeEngine:
+    """Batched InfiniGen decode on one GPU (or one head shard of a TP group).
+
+    Parameters
+    ----------
+    model : object shaped like the reference Model (see model.py)
+    config : RunConfig
+    max_steps : decode steps to size the pool for (default config.gen_len)
+    pool_dtype : "f16" (default, e = 2 bytes), "bf16" or "f32"
+    group : torch.distributed process group for head tensor parallelism
+    fetch_ctas : CTAs of the zero-copy gather (the rest of the GPU computes)
+    """
+
+    def __init__(self, model, config: RunConfig, *, max_steps: int | None = None,
+                 pool_dtype: str = "f16", device=None, group=None, fetch_ctas: int = 32):
+        config.validate()
+        _lib.load()
+        _enable_ieee_fp32()
+        scheme = getattr(config.scheme, "value", config.scheme)
+        if scheme == "speculative" and not getattr(model, "skewed", False):
+            raise ValueError("the speculative scheme requires a skewed model")
+        spec = model.spec
+        self.model, self.config, self.spec, self.scheme = model, config, spec, scheme
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.group = group
+        self.world = dist.get_world_size(group) if group is not None else 1
+        self.rank = dist.get_rank(group) if group is not None else 0
+        H, D, d, L = spec.heads, spec.model_dim, spec.head_dim, spec.layers
+        if H % self.world:
+            raise ValueError(f"{H} heads do not shard over {self.world} ranks")
+        self.H, self.D, self.d, self.L, self.F = H, D, d, L, spec.ffn_dim
+        self.Hg = H // self.world
+        self.h0 = self.rank * self.Hg
+        self.B = config.batch
+        self.elt = pool_dtype
+        self.row_bytes = 2 * d * _lib.ELT_BYTES[pool_dtype]
+        if self.row_bytes % 16:
+            raise ValueError("2*head_dim*element bytes must be a multiple of 16")
+        steps = config.gen_len if max_steps is None else max_steps
+        rows = config.prompt_len + steps
+        if config.pool_limit is not None:
+            rows = min(rows, config.pool_limit)
+        self.S_max = (rows + 3) // 4 * 4
+        sc = config.speculation
+        self.kcols = int(math.ceil(sc.partial_ratio * d))
+        self.cap = max(int(math.floor(sc.cap_ratio * self.S_max)), sc.min_select, 1)
+        self.policy = EvictionPolicy(config.pool_policy)
+        self.fetch_ctas = fetch_ctas
+        self.scale = float(np.float32(1.0 / np.sqrt(d)))   # speculation.py:127
+        self._load_weights(model)
+        self._alloc()
+        self.s_host = 0
+        self.iteration = 0
+        self.records: list = []       # per iteration: [B][L] record dicts
+        self.prefill_info: dict = {}
+        self._prefetched0 = False
+
+    # ------------------------------------------------------------------ setup
+    def _load_weights(self, model) -> None:
+        dev, d, Hg, h0 = self.device, self.d, self.Hg, self.h0
+        c0, c1 = h0 * d, (h0 + Hg) * d
+        self.wqkv, self.wo, self.ffn_in, self.ffn_out, self.ln = [], [], [], [], []
+        for lw in model.layers:
+            q, k, v = (_f32(getattr(lw, f), dev) for f in ("w_q", "w_k", "w_v"))
+            self.wqkv.append(torch.cat([q[:, c0:c1], k[:, c0:c1], v[:, c0:c1]], dim=1).contiguous())
+            self.wo.append(_f32(lw.w_o, dev)[c0:c1].contiguous())
+            self.ffn_in.append(_f32(lw.ffn_in, dev))
+            self.ffn_out.append(_f32(lw.ffn_out, dev))
+            self.ln.append(tuple(_f32(getattr(lw, f), dev) for f in
+                                 ("ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias")))
+
+    def _alloc(self) -> None:
+        dev, B, L, Hg, d, S, cap = self.device, self.B, self.L, self.Hg, self.d, self.S_max, self.cap
+        D, F, kc = self.D, self.F, self.kcols
+        i32, i64, f32 = torch.int32, torch.int64, torch.float32
+        pool_bytes = L * B * Hg * S * self.row_bytes
+        self.pool = HostPool(pool_bytes)
+        self.layer_bytes = B * Hg * S * self.row_bytes
+        spec_ = self.scheme == "speculative"
+        self.pk = torch.zeros((max(L - 1, 1), B, Hg, kc, S), dtype=f32, device=dev) if spec_ else None
+        self.cols = torch.zeros((L, B, Hg, kc), dtype=i32, device=dev)
+        self.arrival = torch.zeros((L, B, Hg, S), dtype=i64, device=dev)
+        self.lastf = torch.zeros((L, B, Hg, S), dtype=i64, device=dev)
+        self.counter = torch.zeros((L, B, Hg, S), dtype=torch.uint8, device=dev)
+        self.st = torch.zeros(8, dtype=i32, device=dev)           # ig_step_state (24 B used)
+        self.xbuf = [torch.zeros((B, D), dtype=f32, device=dev) for _ in range(2)]
+        self.x = self.xbuf[0]
+        self.x_a = torch.empty((B, D), dtype=f32, device=dev)
+        self.x_f = torch.empty((B, D), dtype=f32, device=dev)
+        self.qspec = torch.empty((B, Hg * d), dtype=f32, device=dev)
+        self.qkv = torch.empty((B, 3 * Hg * d), dtype=f32, device=dev)
+        self.attn = torch.empty((B, Hg * d), dtype=f32, device=dev)
+        self.o = torch.empty((B, D), dtype=f32, device=dev)
+        self.hidden = torch.empty((B, F), dtype=f32, device=dev)
+        self.scores = torch.empty((B, Hg, S), dtype=f32, device=dev)
+        self.maxkey = torch.zeros((L, B, Hg), dtype=i32, device=dev)
+        self.counts = torch.zeros((B, Hg), dtype=i32, device=dev)
+        self.count_sum = torch.zeros((L, B), dtype=i32, device=dev)
+        self.idx = torch.zeros((L, B, Hg, cap), dtype=i32, device=dev)
+        self.n = torch.zeros((L, B), dtype=i32, device=dev)
+        self.err = torch.zeros(1, dtype=i32, device=dev)
+        self.pos = torch.zeros((L, B, Hg), dtype=i32, device=dev)
+        self.events = torch.zeros((L, B, Hg, 2), dtype=i64, device=dev)
+        T = _TORCH_ELT[self.elt]
+        self.stage_full = [torch.empty((B, Hg, S, 2 * d), dtype=T, device=dev)
+                           for _ in range(1 if spec_ else 2)]
+        self.stage_sel = [torch.empty((B, Hg, cap, 2 * d), dtype=T, device=dev)
+                          for _ in range(2 if spec_ else 0)]
+        pf, tk = ctypes.c_size_t(), ctypes.c_size_t()
+        _lib.call("ig_attend_scratch", B, Hg, d, S, ctypes.byref(pf), ctypes.byref(tk), kernels=0)
+        self.att_partial = torch.empty(pf.value, dtype=f32, device=dev)
+        self.att_tickets = torch.zeros(tk.value, dtype=i32, device=dev)
+        self.compute = torch.cuda.Stream(device=dev)
+        self.fetch_stream = torch.cuda.Stream(device=dev)
+        self.ev_sel = [torch.cuda.Event() for _ in range(L)]
+        self.ev_fetch = [torch.cuda.Event() for _ in range(L)]
+        self.ev_att = [torch.cuda.Event() for _ in range(L)]
+        self.ev_step = torch.cuda.Event()
+
+    def _set_state(self, s_len: int, seq: int) -> None:
+        limit = self.config.pool_limit or 0
+        st = np.zeros(8, np.int32)
+        st[0], st[1] = s_len, limit
+        st[2:4] = np.array([seq], np.int64).view(np.int32)
+        self.st.copy_(torch.from_numpy(st))
+        self.s_host = s_len
+
+    def pool_view(self) -> np.ndarray:
+        """Host pool as [L][B][Hg][S_max][2][d] (no copy)."""
+        npdt = {"f32": np.float32, "f16": np.float16, "bf16": np.uint16}[self.elt]
+        return self.pool.numpy(npdt, (self.L, self.B, self.Hg, self.S_max, 2, self.d))
+
+    def _pool_layer_dev(self, li: int) -> int:
+        return self.pool.dev + li * self.layer_bytes
+
+    def _pool_layer_host(self, li: int) -> int:
+        return self.pool.host + li * self.layer_bytes
+
+    # ---------------------------------------------------------- state import
+    def load_state(self, x, kv, columns=None, meta=None) -> None:
+        """Inject decode state without prefill ("state injection").
+
+        x: [B, D]; kv(li, b, h) -> (K [s, d], V [s, d]) for GLOBAL head h;
+        columns(li, b, h) -> partial columns for li >= 1; meta(li, b, h) ->
+        (arrival, last_fetch, counter, seq) or None for "s plain appends".
+        """
+        L, B, Hg, d, S = self.L, self.B, self.Hg, self.d, self.S_max
+        pv = self.pool_view()
+        s_len, seq0 = None, None
+        arr = np.zeros((L, B, Hg, S), np.int64)
+        lf = np.zeros((L, B, Hg, S), np.int64)
+        ct = np.zeros((L, B, Hg, S), np.uint8)
+        cols = np.zeros((L, B, Hg, self.kcols), np.int32)
+        for li in range(L):
+            for b in range(B):
+                for hl in range(Hg):
+                    h = self.h0 + hl
+                    K, V = (np.asarray(a, dtype=np.float32) for a in kv(li, b, h))
+                    s = K.shape[0]
+                    if s_len is None:
+                        s_len = s
+                    if s != s_len or s > S:
+                        raise ValueError("all pools must hold the same row count <= S_max")
+                    if self.elt == "bf16":
+                        kb = torch.from_numpy(K).to(torch.bfloat16).view(torch.uint16).numpy()
+                        vb = torch.from_numpy(V).to(torch.bfloat16).view(torch.uint16).numpy()
+                        pv[li, b, hl, :s, 0], pv[li, b, hl, :s, 1] = kb, vb
+                    else:
+                        pv[li, b, hl, :s, 0], pv[li, b, hl, :s, 1] = K, V
+                    if meta is not None and meta(li, b, h) is not None:
+                        a_, l_, c_, sq = meta(li, b, h)
+                        arr[li, b, hl, :s], lf[li, b, hl, :s], ct[li, b, hl, :s] = a_, l_, c_
+                        seq0 = sq
+                    else:
+                        arr[li, b, hl, :s] = np.arange(1, s + 1)
+                        lf[li, b, hl, :s] = np.arange(1, s + 1)
+                        seq0 = s
+                    if li >= 1 and self.scheme == "speculative":
+                        c = np.asarray(columns(li, b, h), dtype=np.int64)
+                        if c.shape != (self.kcols,):
+                            raise ValueError(f"expected {self.kcols} partial columns, got {c.shape}")
+                        cols[li, b, hl] = c
+                        self.pk[li - 1, b, hl, :, :s] = torch.from_numpy(
+                            np.ascontiguousarray(K[:, c].T)).to(self.device)
+        self.arrival.copy_(torch.from_numpy(arr))
+        self.lastf.copy_(torch.from_numpy(lf))
+        self.counter.copy_(torch.from_numpy(ct))
+        self.cols.copy_(torch.from_numpy(cols))
+        self.x.copy_(_f32(x, self.device).reshape(self.B, self.D))
+        self._set_state(s_len, seq0)
+        self._prefetched0 = False
+        torch.cuda.synchronize(self.device)
+
+    @classmethod
+    def from_sessions(cls, model, config: RunConfig, sessions, **kw) -> "DecodeEngine":
+        """Take over reference (or look-alike) DecodeSession objects after their
+        prefill: pools[li][h].keys/values/arrival_seq/last_fetch_seq/
+        fetch_counter/_seq, artifacts.head(li, h).column_indices, x."""
+        eng = cls(model, config, **kw)
+        def kv(li, b, h):
+            p = sessions[b].pools[li][h]
+            return p.keys, p.values
+        def cols(li, b, h):
+            return sessions[b].artifacts.head(li, h).column_indices
+        def meta(li, b, h):
+            p = sessions[b].pools[li][h]
+            return p.arrival_seq, p.last_fetch_seq, p.fetch_counter, p._seq
+        x = np.concatenate([np.asarray(s.x, np.float32).reshape(1, -1) for s in sessions])
+        eng.load_state(x, kv, cols if eng.scheme == "speculative" else None, meta)
+        eng.iteration = sessions[0].iteration
+        return eng
+
+    # ---------------------------------------------------------------- prefill
+    @torch.no_grad()
+    def prefill(self, prompts, tf32: bool = False) -> None:
+        """GPU prefill of all B prompts (engine.py:245-291).  prompts: [B, N, D].
+
+        tf32=True runs the prefill GEMMs on TF32 tensor cores (bench setup of
+        the 13B-class shapes); the default keeps IEEE fp32 like the reference.
+        """
+        cfg, spec = self.config, self.spec
+        L, B, Hg, d, S, D = self.L, self.B, self.Hg, self.d, self.S_max, self.D
+        N = cfg.prompt_len
+        prompts = _f32(prompts, self.device).reshape(B, N, D)
+        row_of, arr, lf, ct, ovw = _simulate_prefill_rows(N, cfg.pool_limit, self.policy)
+        keep_tok = np.full(len(arr), -1, np.int64)
+        for t, r in enumerate(row_of):
+            keep_tok[r] = t                       # last token written to each row
+        rows = len(arr)
+        keep = torch.from_numpy(keep_tok).to(self.device)
+        T = _TORCH_ELT[self.elt]
+        old = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = bool(tf32)
+        try:
+            for b in range(B):
+                x = prompts[b]
+                for li in range(L):
+                    g1, b1, g2, b2 = self.ln[li]
+                    x_a = layernorm(x, g1, b1, spec.ln_eps)
+                    qkv = x_a @ self.wqkv[li]
+                    q, k, v = (qkv[:, i * Hg * d:(i + 1) * Hg * d].reshape(N, Hg, d).transpose(0, 1)
+                               for i in range(3))
+                    att = causal_attention(q.contiguous(), k.contiguous(), v.contiguous())
+                    o = att.transpose(0, 1).reshape(N, Hg * d) @ self.wo[li]
+                    if self.world > 1:
+                        dist.all_reduce(o, group=self.group)
+                    mid = x + o
+                    xf = layernorm(mid, g2, b2, spec.ln_eps)
+                    x = mid + torch.relu(xf @ self.ffn_in[li]) @ self.ffn_out[li]
+                    # pool rows (keep_tok: which prompt token survives in each row)
+                    kvrows = torch.stack([k[:, keep], v[:, keep]], dim=2).to(T).contiguous()
+                    base = self._pool_layer_host(li) + b * Hg * S * self.row_bytes
+                    _lib.call("ig_memcpy2d", base, S * self.row_bytes, kvrows.data_ptr(),
+                              rows * self.row_bytes, rows * self.row_bytes, Hg,
+                              _lib.stream_handle(), kernels=0)
+                    if li >= 1 and self.scheme == "speculative":
+                        cols = partial_columns(q, k, cfg.speculation.partial_ratio)
+                        self.cols[li, b] = cols
+                        ksel = torch.gather(k[:, keep], 2, cols.long()[:, None, :].expand(Hg, rows, self.kcols))
+                        self.pk[li - 1, b, :, :, :rows] = ksel.transpose(1, 2)
+                    torch.cuda.current_stream().synchronize()  # kvrows lifetime
+                self.x[b] = x[-1]
+        finally:
+            torch.backends.cuda.matmul.allow_tf32 = old
+        self.arrival[..., :rows] = torch.from_numpy(arr).to(self.device)
+        self.lastf[..., :rows] = torch.from_numpy(lf).to(self.device)
+        self.counter[..., :rows] = torch.from_numpy(ct).to(self.device)
+        self._set_state(rows, N)
+        self._prefetched0 = False
+        self.prefill_info = {"prompt_len": N, "pool_rows": rows,
+                             "partial_cols": self.kcols if (self.scheme == "speculative" and L > 1) else None,
+                             "pool_overwrites": ovw * L * self.H}
+        torch.cuda.synchronize(self.device)
+
+    # ----------------------------------------------------------------- decode
+    def _issue_full_fetch(self, li: int, s: int, stage: torch.Tensor) -> None:
+        _lib.call("ig_fetch_all", self._pool_layer_host(li), self.B, self.Hg, self.S_max, s,
+                  self.row_bytes, stage.data_ptr(), self.S_max,
+                  self.fetch_stream.cuda_stream, kernels=0)
+
+    def _attend(self, li: int, stage, idx, n, stage_rows: int, cs: int) -> None:
+        Hgd = self.Hg * self.d
+        q = self.qkv
+        _lib.call("ig_attend", q.data_ptr(), 3 * Hgd, q.data_ptr() + 4 * Hgd,
+                  q.data_ptr() + 8 * Hgd, 3 * Hgd, stage.data_ptr(), _lib.ELT[self.elt],
+                  _lib.ptr(idx), _lib.ptr(n), self.pos[li].data_ptr(), self.st.data_ptr(),
+                  self.B, self.Hg, self.d, stage_rows, self.att_partial.data_ptr(),
+                  self.att_tickets.data_ptr(), self.attn.data_ptr(), Hgd, cs)
+
+    @torch.no_grad()
+    def decode_step(self) -> torch.Tensor:
+        """One decode iteration for all B sequences; returns x [B, D] on the
+        device (an engine buffer: valid until the next decode_step)."""
+        if self.s_host < 1:
+            raise RuntimeError("prefill has not run")
+        cfg, spec = self.config, self.spec
+        L, B, Hg, d = self.L, self.B, self.Hg, self.d
+        Hgd = Hg * d
+        speculative = self.scheme == "speculative"
+        sc = cfg.speculation
+        C, Fs = self.compute, self.fetch_stream
+        cs = C.cuda_stream
+        s = self.s_host
+        recording = cfg.record_selection or cfg.record_scores
+        recs = [[None] * L for _ in range(B)]
+        spec_scores = [None] * L
+        C.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(C):
+            self.maxkey.zero_()
+            self.count_sum.zero_()
+            self.ev_step.record(C)
+            if not self._prefetched0:
+                Fs.wait_event(self.ev_step)
+                self._issue_full_fetch(0, s, self.stage_full[0])
+                self.ev_fetch[0].record(Fs)
+            x = self.x
+            for li in range(L):
+                g1, b1, g2, b2 = self.ln[li]
+                _lib.call("ig_layernorm", x.data_ptr(), g1.data_ptr(), b1.data_ptr(),
+                          float(spec.ln_eps), B, self.D, self.x_a.data_ptr(), cs)
+                nxt = li + 1
+                if nxt < L:
+                    if speculative:
+                        torch.matmul(self.x_a, self.wqkv[nxt][:, :Hgd], out=self.qspec)
+                        _lib.call("ig_rehearse", self.qspec.data_ptr(), Hgd,
+                                  self.cols[nxt].data_ptr(), self.pk[nxt - 1].data_ptr(),
+                                  self.st.data_ptr(), B, Hg, d, self.kcols, self.S_max,
+                                  self.scale, self.scores.data_ptr(),
+                                  self.maxkey[nxt].data_ptr(), cs)
+                        _lib.call("ig_count", self.scores.data_ptr(), self.maxkey[nxt].data_ptr(),
+                                  self.st.data_ptr(), B, Hg, self.S_max, float(sc.alpha),
+                                  self.counts.data_ptr(), self.count_sum[nxt].data_ptr(), cs)
+                        if self.world > 1:
+                            dist.all_reduce(self.count_sum[nxt], group=self.group)
+                        _lib.call("ig_select", self.scores.data_ptr(),
+                                  self.count_sum[nxt].data_ptr(), self.st.data_ptr(), B, Hg,
+                                  self.H, self.S_max, self.cap, float(sc.cap_ratio),
+                                  int(sc.min_select), self.idx[nxt].data_ptr(),
+                                  self.n[nxt].data_ptr(), self.err.data_ptr(), cs)
+                        if cfg.record_scores:
+                            spec_scores[nxt] = self.scores[:, :, :s].cpu()
+                        self.ev_sel[nxt].record(C)
+                        Fs.wait_event(self.ev_sel[nxt])
+                        _lib.call("ig_fetch", self._pool_layer_dev(nxt), self.idx[nxt].data_ptr(),
+                                  self.n[nxt].data_ptr(), B, Hg, self.S_max, self.cap,
+                                  self.row_bytes, self.stage_sel[nxt % 2].data_ptr(),
+                                  self.fetch_ctas, Fs.cuda_stream)
+                    else:
+                        if li >= 1:
+                            Fs.wait_event(self.ev_att[li - 1])
+                        else:
+                            Fs.wait_event(self.ev_step)
+                        self._issue_full_fetch(nxt, s, self.stage_full[nxt % 2])
+                    self.ev_fetch[nxt].record(Fs)
+                torch.matmul(self.x_a, self.wqkv[li], out=self.qkv)
+                sel = speculative and li >= 1
+                _lib.call("ig_append", self.qkv.data_ptr() + 4 * Hgd, self.qkv.data_ptr() + 8 * Hgd,
+                          3 * Hgd, self._pool_layer_dev(li), _lib.ELT[self.elt],
+                          _lib.ptr(self.pk[li - 1]) if sel else None,
+                          _lib.ptr(self.cols[li]) if sel else None, self.kcols,
+                          self.arrival[li].data_ptr(), self.lastf[li].data_ptr(),
+                          self.counter[li].data_ptr(), _lib.POLICY[self.policy.value],
+                          2 if sel else 1, _lib.ptr(self.idx[li]) if sel else None,
+                          _lib.ptr(self.n[li]) if sel else None, self.cap,
+                          self.st.data_ptr(), B, Hg, d, self.S_max, self.pos[li].data_ptr(),
+                          self.events[li].data_ptr(), cs)
+                C.wait_event(self.ev_fetch[li])
+                if sel:
+                    self._attend(li, self.stage_sel[li % 2], self.idx[li], self.n[li], self.cap, cs)
+                else:
+                    stage = self.stage_full[0] if speculative else self.stage_full[li % 2]
+                    self._attend(li, stage, None, None, self.S_max, cs)
+                self.ev_att[li].record(C)
+                torch.matmul(self.attn, self.wo[li], out=self.o)
+                if self.world > 1:
+                    dist.all_reduce(self.o, group=self.group)
+                self.o.add_(x)                                  # x_mid = x + attn_out
+                _lib.call("ig_layernorm", self.o.data_ptr(), g2.data_ptr(), b2.data_ptr(),
+                          float(spec.ln_eps), B, self.D, self.x_f.data_ptr(), cs)
+                torch.matmul(self.x_f, self.ffn_in[li], out=self.hidden)
+                self.hidden.relu_()
+                x_new = self.xbuf[1] if x is self.xbuf[0] else self.xbuf[0]
+                torch.addmm(self.o, self.hidden, self.ffn_out[li], out=x_new)
+                if recording:
+                    self._record(li, s, recs, spec_scores)
+                x = x_new
+            _lib.call("ig_step_advance", self.st.data_ptr(), cs)
+            s_next = min(s + 1, cfg.pool_limit) if cfg.pool_limit else s + 1
+            # next step's layer-0 rows stream in while the tail of this step runs
+            # (after the last attend that reads stage_full[0])
+            last0 = 0 if speculative else (L - 1 if (L - 1) % 2 == 0 else L - 2)
+            Fs.wait_event(self.ev_att[last0])
+            self._issue_full_fetch(0, s_next, self.stage_full[0])
+            self.ev_fetch[0].record(Fs)
+            self._prefetched0 = True
+            self.x = x
+        torch.cuda.current_stream(self.device).wait_stream(C)
+        self.s_host = s_next
+        if speculative and L > 1 and int(self.err.item() if recording else 0):
+            raise RuntimeError("selection exceeded the index buffer (cap)")
+        if recording:
+            self.records.append([recs[b] for b in range(B)])
+        self.iteration += 1
+        return x
+
+    def _record(self, li, s, recs, spec_scores) -> None:
+        """LayerRecord fields (engine.py:420-446) for every sequence."""
+        torch.cuda.synchronize(self.device)
+        cfg, spec = self.config, self.spec
+        H, d, bpe = self.H, self.d, cfg.kv_bytes_per_element
+        speculative = self.scheme == "speculative"
+        pos = self.pos[li].cpu().numpy()
+        ev = self.events[li].cpu().numpy()
+        n_dev = self.n[li].cpu().numpy()
+        idx = self.idx[li].cpu().numpy()
+        for b in range(self.B):
+            n_sel = int(n_dev[b]) if (speculative and li >= 1) else s
+            sflops = 0.0
+            if speculative and li + 1 < self.L:
+                sflops = float(H * (2 * self.D * self.kcols + 2 * self.kcols * s))
+            r = {"iteration": self.iteration, "layer": li, "n_selected": n_sel,
+                 "bytes": selection_bytes(n_sel, H, d, bpe),
+                 "full_bytes": selection_bytes(s, H, d, bpe),
+                 "attention_flops": float(H * 4 * n_sel * d),
+                 "ffn_flops": float(2 * self.D * self.F * 2),
+                 "speculation_flops": sflops,
+                 "pool_events": [{"layer": li, "head": self.h0 + h, "victim": int(ev[b, h, 0]),
+                                  "arrival_seq": int(ev[b, h, 1])}
+                                 for h in range(self.Hg) if ev[b, h, 0] >= 0]}
+            if cfg.record_selection:
+                sel = []
+                for h in range(self.Hg):
+                    if speculative and li >= 1:
+                        rows = idx[b, h, :n_sel]
+                    else:
+                        rows = np.arange(s + (0 if (cfg.pool_limit and s >= cfg.pool_limit) else 1))
+                    sel.append(sorted(int(i) for i in rows if i != pos[b, h]))
+                r["selected"] = sel
+            if cfg.record_scores and speculative and li >= 1 and spec_scores[li] is not None:
+                r["spec_scores"] = [[float(v) for v in spec_scores[li][b, h].tolist()]
+                                    for h in range(self.Hg)]
+            recs[b][li] = r
+
+    def step_host(self, x_host: np.ndarray | None = None) -> np.ndarray:
+        """End-to-end API: optional host input row(s) in, host output rows out
+        (the reference decode_step returns the output row, engine.py:380)."""
+        if x_host is not None:
+            self.x.copy_(torch.from_numpy(np.ascontiguousarray(x_host, np.float32)).reshape(self.B, self.D),
+                         non_blocking=True)
+        return self.decode_step().cpu().numpy()
+
+    def trace(self) -> dict:
+        """Schema-v1 trace (engine.py:83-196; selected lists are ascending)."""
+        cfg = self.config
+        return {"version": TRACE_SCHEMA_VERSION, "scheme": self.scheme, "layers": self.L,
+                "heads": self.H, "head_dim": self.d,
+                "config": {"scheme": self.scheme, "prompt_len": cfg.prompt_len,
+                           "gen_len": cfg.gen_len, "batch": cfg.batch,
+                           "partial_ratio": cfg.speculation.partial_ratio,
+                           "alpha": cfg.speculation.alpha, "cap_ratio": cfg.speculation.cap_ratio,
+                           "min_select": cfg.speculation.min_select,
+                           "pool_limit": cfg.pool_limit, "pool_policy": self.policy.value,
+                           "prompt_seed": cfg.prompt_seed,
+                           "kv_bytes_per_element": cfg.kv_bytes_per_element},
+                "sequences": [{"prefill": dict(self.prefill_info),
+                               "iterations": [it[b] for it in self.records]}
+                              for b in range(self.B)]}
+
+    def close(self) -> None:
+        self.pool.close()
+
+
+def run(model, config: RunConfig, *, prompts=None, **kw):
+    """Reference run() (engine.py:456-477) on the B200 path: prefill + gen_len
+    decode steps for the whole batch at once.  prompts defaults to the
+    reference's seeded normals random_prompt(N, D, prompt_seed + b)."""
+    D = model.spec.model_dim
+    if prompts is None:
+        prompts = np.stack([np.random.default_rng(config.prompt_seed + b)
+                            .standard_normal((config.prompt_len, D)).astype(np.float32)
+                            for b in range(config.batch)])
+    eng = DecodeEngine(model, config, **kw)
+    try:
+        eng.prefill(prompts)
+        out = eng.x.cpu().numpy()
+        for _ in range(config.gen_len):
+            out = eng.decode_step().cpu().numpy()
+        return eng.trace(), [out[b].copy() for b in range(config.batch)]
+    finally:
+        eng.close()

@@ -1,0 +1,223 @@
+"""Decode-path parity on the GPU: the batched B200 engine vs the oracle.
+
+* drop-in hook mode: the oracle's own decode loop (engine.py:295-380
+  restated) with the GPU shims plugged in by name, checked call by call;
+* engine mode, f32 pool: from the oracle's prefill state, every decode
+  step's output rows within 1e-4 (scaled), every (seq, layer, head) selected
+  set, n, bytes and pool-eviction event identical;
+* engine mode, f16 pool (the product default, e = 2 bytes): outputs within
+  5e-3 relative, selections agreeing >= 97% (fp16 K/V legitimately move
+  x and therefore later selections -- SURVEY.md s7 hard part 1);
+* GPU prefill vs the oracle prefill; AC12 identity; batch independence.
+"""
+
+import copy
+
+import numpy as np
+import pytest
+
+from oracle import speckv_port as O
+from tests.golden_cfg import MODELS, RUNS, models, run_config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2406_19707_b200 import _lib
+    _lib.load()
+
+
+def engine_cfg(ocfg, **kw):
+    from paper_2406_19707_b200 import RunConfig, SpeculationConfig
+    from paper_2406_19707_b200.pool import EvictionPolicy
+    s = ocfg.speculation
+    base = dict(scheme=ocfg.scheme, prompt_len=ocfg.prompt_len, gen_len=ocfg.gen_len,
+                batch=ocfg.batch,
+                speculation=SpeculationConfig(s.partial_ratio, s.alpha, s.cap_ratio, s.min_select),
+                pool_limit=ocfg.pool_limit, pool_policy=EvictionPolicy(O.Policy(ocfg.pool_policy).value),
+                prompt_seed=ocfg.prompt_seed, kv_bytes_per_element=ocfg.kv_bytes_per_element,
+                record_selection=True)
+    base.update(kw)
+    return RunConfig(**base)
+
+
+def oracle_sessions(model, cfg):
+    D = model.spec.model_dim
+    return [O.Session(model, cfg, O.random_prompt(cfg.prompt_len, D, cfg.prompt_seed + b))
+            for b in range(cfg.batch)]
+
+
+def oracle_decode(sessions, steps):
+    outs = [[s.x[0].copy()] for s in sessions]
+    for _ in range(steps):
+        for b, s in enumerate(sessions):
+            outs[b].append(s.decode_step())
+    return np.array(outs), [s.records for s in sessions]
+
+
+def _cmp_records(eng_recs, ref_recs, B, exact=True):
+    """eng_recs: [iter][b][layer]; ref_recs: [b][iter][layer].  Returns the
+    selection agreement (|A & B| / |B| summed) over all (it, b, layer, head)."""
+    hit = tot = 0
+    for it, per_b in enumerate(eng_recs):
+        for b in range(B):
+            for li, r in enumerate(per_b[b]):
+                rr = ref_recs[b][it][li]
+                if exact:
+                    for key in ("n_selected", "bytes", "full_bytes", "pool_events"):
+                        assert r[key] == rr[key], (key, it, b, li)
+                for h, (sel, rsel) in enumerate(zip(r["selected"], rr["selected"])):
+                    a, c = set(sel), set(rsel)
+                    if exact:
+                        assert a == c, (it, b, li, h, sorted(a ^ c))
+                    hit += len(a & c)
+                    tot += max(len(c), 1)
+    return hit / max(tot, 1)
+
+
+def _scaled_err(a, b):
+    return float(np.abs(a - b).max() / max(1.0, np.abs(b).max()))
+
+
+@pytest.mark.parametrize("rname", sorted(RUNS))
+@pytest.mark.parametrize("mname", sorted(MODELS))
+def test_engine_f32_pool_matches_oracle(mname, rname):
+    from paper_2406_19707_b200 import DecodeEngine
+    plain, sk = models(mname)
+    ocfg = run_config(rname, record_selection=True)
+    model = sk if ocfg.scheme == "speculative" else plain
+    sessions = oracle_sessions(model, ocfg)
+    eng = DecodeEngine.from_sessions(model, engine_cfg(ocfg), copy.deepcopy(sessions), pool_dtype="f32")
+    try:
+        ref_out, ref_recs = oracle_decode(sessions, ocfg.gen_len)
+        got = [eng.x.cpu().numpy()]
+        for _ in range(ocfg.gen_len):
+            got.append(eng.decode_step().cpu().numpy())
+        got = np.stack(got, axis=1)                      # [B][T+1][D]
+        assert _scaled_err(got, ref_out) < 1e-4
+        _cmp_records(eng.records, ref_recs, ocfg.batch, exact=True)
+        # pool metadata after the run is the reference's, exactly
+        for li in range(model.spec.layers):
+            for b in range(ocfg.batch):
+                for h in range(model.spec.heads):
+                    p = sessions[b].pools[li][h]
+                    s = len(p)
+                    np.testing.assert_array_equal(eng.arrival[li, b, h, :s].cpu().numpy(), p.arrival_seq)
+                    np.testing.assert_array_equal(eng.lastf[li, b, h, :s].cpu().numpy(), p.last_fetch_seq)
+                    np.testing.assert_array_equal(eng.counter[li, b, h, :s].cpu().numpy(), p.fetch_counter)
+        pv = eng.pool_view()
+        p = sessions[0].pools[1][0]
+        np.testing.assert_allclose(pv[1, 0, 0, :len(p), 0], p.keys, rtol=1e-5, atol=1e-5)
+    finally:
+        eng.close()
+
+
+@pytest.mark.parametrize("mname", sorted(MODELS))
+def test_engine_f16_pool_tolerance(mname):
+    from paper_2406_19707_b200 import DecodeEngine
+    _, sk = models(mname)
+    ocfg = run_config("spec", record_selection=True)
+    sessions = oracle_sessions(sk, ocfg)
+    eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg), copy.deepcopy(sessions), pool_dtype="f16")
+    try:
+        ref_out, ref_recs = oracle_decode(sessions, ocfg.gen_len)
+        got = np.stack([eng.x.cpu().numpy()] + [eng.decode_step().cpu().numpy()
+                                                for _ in range(ocfg.gen_len)], axis=1)
+        assert _scaled_err(got, ref_out) < 5e-3
+        assert _cmp_records(eng.records, ref_recs, ocfg.batch, exact=False) >= 0.97
+    finally:
+        eng.close()
+
+
+def test_hook_mode_drop_in(monkeypatch):
+    """The reference decode loop with the GPU operators plugged in by name;
+    every call is checked against the oracle operator on identical inputs."""
+    import paper_2406_19707_b200 as G
+    _, sk = models("m64")
+    ocfg = run_config("spec_counter", record_selection=True)
+    calls = {"spec": 0, "sel": 0, "attn": 0}
+
+    def spec_hook(x, arts, layer, d):
+        got, ref = G.speculate_scores(x, arts, layer, d), O.speculate_scores(x, arts, layer, d)
+        for g, r in zip(got, ref):
+            np.testing.assert_allclose(g, r, rtol=1e-5, atol=1e-5)
+        calls["spec"] += 1
+        return ref
+
+    def sel_hook(scores, cfg):
+        got, ref = G.select_tokens(scores, cfg), O.select_tokens(scores, cfg)
+        assert got[1] == ref[1]
+        for g, r in zip(got[0], ref[0]):
+            np.testing.assert_array_equal(g, r)
+        calls["sel"] += 1
+        return ref
+
+    def attn_hook(q, k, v):
+        (go, _), (ro, rw) = G.attention_head(q, k, v), O.attention_head(q, k, v)
+        np.testing.assert_allclose(go, ro, rtol=1e-5, atol=1e-5)
+        calls["attn"] += 1
+        return ro, rw
+
+    sess = O.Session(sk, ocfg, O.random_prompt(ocfg.prompt_len, 64, 0),
+                     hooks={"speculate_scores": spec_hook, "select_tokens": sel_hook,
+                            "attention_head": attn_hook})
+    for _ in range(4):
+        sess.decode_step()
+    assert calls["spec"] == 4 * 2 and calls["sel"] == 4 * 2 and calls["attn"] == 4 * 3 * 4
+
+
+def test_gpu_prefill_matches_oracle():
+    from paper_2406_19707_b200 import DecodeEngine
+    _, sk = models("m256")
+    ocfg = run_config("spec", record_selection=True)
+    sessions = oracle_sessions(sk, ocfg)
+    eng = DecodeEngine(sk, engine_cfg(ocfg), pool_dtype="f32")
+    try:
+        prompts = np.stack([O.random_prompt(ocfg.prompt_len, 256, ocfg.prompt_seed + b)
+                            for b in range(ocfg.batch)])
+        eng.prefill(prompts)
+        assert eng.prefill_info == sessions[0].prefill_info
+        pv = eng.pool_view()
+        for li in range(3):
+            for b in range(ocfg.batch):
+                for h in range(2):
+                    p = sessions[b].pools[li][h]
+                    np.testing.assert_allclose(pv[li, b, h, :len(p), 0], p.keys, rtol=1e-4, atol=1e-4)
+                    np.testing.assert_allclose(pv[li, b, h, :len(p), 1], p.values, rtol=1e-4, atol=1e-4)
+                    if li >= 1:
+                        np.testing.assert_array_equal(eng.cols[li, b, h].cpu().numpy(),
+                                                      sessions[b].artifacts.head(li, h).column_indices)
+        x_ref = np.concatenate([s.x for s in sessions])
+        assert _scaled_err(eng.x.cpu().numpy(), x_ref) < 1e-4
+        ref_out, ref_recs = oracle_decode(sessions, 3)
+        got = np.stack([eng.x.cpu().numpy()] + [eng.decode_step().cpu().numpy() for _ in range(3)], axis=1)
+        assert _scaled_err(got, ref_out) < 1e-3
+        assert _cmp_records(eng.records, ref_recs, ocfg.batch, exact=False) >= 0.97
+    finally:
+        eng.close()
+
+
+def test_ac12_identity_speculative_equals_full():
+    """alpha -> inf, cap 1.0, no limit: speculative == full (SPEC.md AC12)."""
+    from paper_2406_19707_b200 import run
+    plain, sk = models("m64")
+    base = run_config("spec_identity")
+    tr_s, out_s = run(sk, engine_cfg(base), pool_dtype="f32")
+    tr_f, out_f = run(plain, engine_cfg(base, scheme="full"), pool_dtype="f32")
+    assert _scaled_err(np.stack(out_s), np.stack(out_f)) < 1e-3
+
+
+def test_batch_rows_are_independent():
+    """Sequence b of a batch-4 run equals the same prompt run alone."""
+    from paper_2406_19707_b200 import run
+    _, sk = models("m64")
+    ocfg = run_config("spec", batch=4, gen_len=3)
+    _, outs = run(sk, engine_cfg(ocfg), pool_dtype="f32")
+    for b in (0, 3):
+        single = engine_cfg(ocfg, batch=1, prompt_seed=b)
+        _, one = run(sk, single, pool_dtype="f32")
+        assert _scaled_err(outs[b], one[0]) < 1e-5

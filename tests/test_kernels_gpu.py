@@ -1,0 +1,162 @@
+"""Operator-level parity on the GPU: each drop-in shim (reference signature) vs
+the oracle and the reference's golden vectors.
+
+Bars: indices / n / pool metadata bit-exact; rehearsal scores rtol 1e-5;
+attention (f32) rtol 1e-5; layernorm rtol 1e-6.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import speckv_port as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2406_19707_b200 as pk  # noqa: F401  (raises if the library is missing)
+    from paper_2406_19707_b200 import _lib
+    _lib.load()
+
+
+def test_select_tokens_golden_bit_exact(golden):
+    from paper_2406_19707_b200 import SpeculationConfig, select_tokens
+    for case in golden["ops"]["select"]:
+        if "case" not in case:
+            continue
+        c = case["case"]
+        sc = golden["arrays"][f"sel.{c}.scores"]
+        cfg = SpeculationConfig(0.3, case["alpha"], case["cap_ratio"], case["min_select"])
+        picks, n = select_tokens([sc[h] for h in range(sc.shape[0])], cfg)
+        assert n == case["n"], c
+        # full list equality: same set AND the reference's stable score order
+        np.testing.assert_array_equal(np.stack(picks), golden["arrays"][f"sel.{c}.picks"])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_select_tokens_random_with_ties(seed):
+    from paper_2406_19707_b200 import SpeculationConfig, select_tokens
+    rng = np.random.default_rng(100 + seed)
+    for _ in range(8):
+        H = int(rng.integers(1, 9))
+        s = int(rng.choice([1, 2, 5, 63, 64, 65, 511, 1500, 4097]))
+        q = float(rng.choice([0.0, 0.5, 0.01]))
+        sc = rng.standard_normal((H, s)).astype(np.float32) * np.float32(rng.choice([0.1, 3.0, 50.0]))
+        if q:
+            sc = (np.round(sc / q) * q).astype(np.float32)
+        sc[:, rng.integers(0, s, size=max(1, s // 10))] = 0.0
+        if s > 3:
+            sc[0, :2] = -0.0                       # -0.0 and +0.0 tie (linalg.py:184)
+        cfg = O.SpeculationConfig(0.3, float(rng.choice([0.25, 1.0, 4.0, 1e9])),
+                                  float(rng.choice([0.01, 0.2, 1.0])), int(rng.choice([1, 3])))
+        ref_p, ref_n = O.select_tokens([sc[h] for h in range(H)], cfg)
+        got_p, got_n = select_tokens([sc[h] for h in range(H)],
+                                     SpeculationConfig(*[getattr(cfg, f) for f in
+                                                         ("partial_ratio", "alpha", "cap_ratio", "min_select")]))
+        assert got_n == ref_n
+        for h in range(H):
+            np.testing.assert_array_equal(got_p[h], ref_p[h])
+
+
+def test_topk_rows_matches_stable_argsort():
+    import torch
+    from paper_2406_19707_b200 import _lib
+    rng = np.random.default_rng(5)
+    for rows, length, k in [(1, 10, 3), (7, 128, 39), (40, 64, 20), (3, 5000, 1000), (2, 33, 33)]:
+        v = np.round(rng.standard_normal((rows, length)) * 4).astype(np.float32)  # many ties
+        dv = torch.from_numpy(v).cuda()
+        out = torch.empty((rows, k), dtype=torch.int32, device="cuda")
+        _lib.call("ig_topk_rows", dv.data_ptr(), rows, length, k, out.data_ptr(), _lib.stream_handle())
+        for r in range(rows):
+            np.testing.assert_array_equal(out[r].cpu().numpy(), np.sort(O.topk_indices(v[r], k)))
+
+
+def test_build_partial_golden(golden):
+    from paper_2406_19707_b200 import build_partial
+    a = golden["arrays"]
+    for case in golden["ops"]["select"]:
+        if "bp_case" not in case:
+            continue
+        c = case["bp_case"]
+        np.testing.assert_array_equal(build_partial(a[f"bp.{c}.qt"], a[f"bp.{c}.kt"], case["ratio"]),
+                                      a[f"bp.{c}.cols"])
+
+
+@pytest.mark.parametrize("s", [1, 3, 4, 1000, 4097])
+def test_speculate_scores_vs_oracle(s):
+    from paper_2406_19707_b200 import speculate_scores
+    rng = np.random.default_rng(s)
+    H, D, d = 4, 64, 16
+    k = 5
+    arts = O.Partials(3, H)
+    for h in range(H):
+        arts.set_head(2, h, O.HeadPartial(np.sort(rng.choice(d, k, replace=False)),
+                                          rng.standard_normal((D, k)).astype(np.float32),
+                                          rng.standard_normal((s, k)).astype(np.float32) * 3))
+    x = rng.standard_normal(D).astype(np.float32)
+    ref = O.speculate_scores(x, arts, 2, d)
+    got = speculate_scores(x, arts, 2, d)
+    for h in range(H):
+        np.testing.assert_allclose(got[h], ref[h], rtol=1e-5, atol=1e-5)
+    with pytest.raises(ValueError):
+        speculate_scores(x, arts, 0, d)
+
+
+def test_attention_head_golden(golden):
+    from paper_2406_19707_b200 import attention_head
+    a = golden["arrays"]
+    for c in range(12):
+        o, w = attention_head(a[f"attn.{c}.q"], a[f"attn.{c}.k"], a[f"attn.{c}.v"])
+        np.testing.assert_allclose(o, a[f"attn.{c}.out"], rtol=1e-5, atol=1e-5)
+        np.testing.assert_allclose(w, a[f"attn.{c}.w"], rtol=1e-5, atol=1e-6)
+    with pytest.raises(ValueError):
+        attention_head(np.zeros((1, 4)), np.zeros((0, 4)), np.zeros((0, 4)))
+
+
+def test_kvpool_golden_logs(golden):
+    from paper_2406_19707_b200 import EvictionPolicy, KvPool
+    for log in golden["ops"]["pool"]:
+        events = []
+        p = KvPool(4, limit=log["limit"], policy=EvictionPolicy(log["policy"]),
+                   on_overwrite=lambda v, a: events.append((v, a)))
+        ref = O.Pool(4, limit=log["limit"], policy=O.Policy(log["policy"]),
+                     on_overwrite=None)
+        for op in log["ops"]:
+            if op[0] == "a":
+                k = np.array(op[1], np.float32)
+                if len(ref) == ref.limit:
+                    assert p.evict_select() == ref.evict_select()
+                assert p.append(k, -k) == op[2]
+                ref.append(k, -k)
+            else:
+                K, V = p.fetch(op[1])
+                assert float(K.sum()) == pytest.approx(op[2], rel=1e-5, abs=1e-5)
+                np.testing.assert_array_equal(V, -K)
+                ref.fetch(op[1])
+        fin = log["final"]
+        np.testing.assert_array_equal(p.arrival_seq, fin["arrival_seq"])
+        np.testing.assert_array_equal(p.last_fetch_seq, fin["last_fetch_seq"])
+        np.testing.assert_array_equal(p.fetch_counter, fin["fetch_counter"])
+        np.testing.assert_array_equal(p.keys, np.array(fin["keys"], np.float32))
+        assert len(events) == max(0, sum(op[0] == "a" for op in log["ops"]) - log["limit"])
+        with pytest.raises(IndexError):
+            p.fetch([len(p)])
+        p.close()
+
+
+def test_layernorm_vs_oracle():
+    import torch
+    from paper_2406_19707_b200.prefill import layernorm
+    rng = np.random.default_rng(9)
+    for rows, D in [(1, 64), (16, 5120), (3, 7168)]:
+        x = (rng.standard_normal((rows, D)) * 3 + 1).astype(np.float32)
+        g = (1 + 0.02 * rng.standard_normal(D)).astype(np.float32)
+        b = (0.02 * rng.standard_normal(D)).astype(np.float32)
+        ref = O.layernorm(x, g, b, 1e-5)
+        got = layernorm(torch.from_numpy(x).cuda(), torch.from_numpy(g).cuda(),
+                        torch.from_numpy(b).cuda(), 1e-5).cpu().numpy()
+        np.testing.assert_allclose(got, ref, rtol=1e-6, atol=2e-6)
