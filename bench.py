@@ -1,0 +1,358 @@
+#!/usr/bin/env python3
+"""Decode-throughput benchmark of the B200 InfiniGen KV path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json metric "decode tok/s (OPT-13B, KV on host)"):
+OPT-13B-shaped decode (40 layers, D 5120, 40 heads, d 128, FFN 20480),
+batch 16, 4096-token prompt (context 4096 + steps), KV pool in pinned host
+memory (fp16, e = 2 B, the reference accounting), speculation ratio 0.3,
+alpha 4, cap 20%.  Weights: random init with the reference's synthetic
+recipe (outlier scale 2.0) drawn by torch's RNG on the GPU; skew by GPU SVD;
+prompts N(0, 1); GPU prefill (TF32) builds the pool -- all outside the timed
+region.  A "step" = one decode iteration of all 16 sequences.
+
+N > 1 (torchrun): heads are sharded over the ranks (each owns H/N heads,
+their pool shard and partial keys); NCCL all-reduces the per-layer head
+counts and W_O output.  Total work is fixed -> "scaling": "strong".
+
+--impl reference times the reference algorithm (the NumPy oracle port; the
+reference is Python, so there is nothing to compile) on the host cores: a
+3-layer truncation of the same shape at the same context with injected
+state, extrapolated to 40 layers and to the serial batch (engine.py:468-476).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = dict(name="OPT-13B-shaped decode, batch 16, 4K context (BASELINE.json configs[2])",
+                shape="opt-13b", batch=16, prompt=4096, alpha=4.0, ratio=0.3, cap=0.2,
+                outlier_scale=2.0)
+METRIC = "decode tok/s (OPT-13B, KV on host)"
+UNIT = "tok/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--batch", type=int, default=WORKLOAD["batch"])
+    ap.add_argument("--prompt", type=int, default=WORKLOAD["prompt"])
+    ap.add_argument("--shape", default=WORKLOAD["shape"])
+    ap.add_argument("--layers", type=int, default=None, help="override (debug only)")
+    ap.add_argument("--fetch-ctas", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self._p = index, [], None
+
+    def __enter__(self):
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                        "-i", str(self.index), "-lms", "200"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self._p = None
+        return self
+
+    def _read(self):
+        for line in self._p.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self._p is not None:
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._p.kill()
+
+    def summary(self) -> dict:
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 9
+                          for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------- reference (CPU)
+def cpu_reference(shape: str, batch: int, prompt: int, steps: int, warmup: int = 1) -> dict:
+    """Time the reference algorithm (oracle port, NumPy/OpenBLAS, all host
+    cores) on a 3-layer truncation of the workload with injected state;
+    extrapolate T_step = T0 + (L-2) * T1 + T_last per sequence, x batch."""
+    import numpy as np
+    from oracle import speckv_port as O
+    from paper_2406_19707_b200.model import SHAPES
+    sh = SHAPES[shape]
+    L_full, D, H, F = sh["layers"], sh["model_dim"], sh["heads"], sh["ffn_dim"]
+    d = D // H
+    Lt = 3
+    rng = np.random.default_rng(0)
+    spec = O.ModelSpec(layers=Lt, model_dim=D, heads=H, ffn_dim=F, outlier_channels=8,
+                       outlier_scale=2.0, seed=0)
+
+    def mat(r, c):
+        return rng.standard_normal((r, c), dtype=np.float32) * np.float32(1.0 / np.sqrt(r))
+
+    layers = []
+    for _ in range(Lt):
+        g = (1 + 0.02 * rng.standard_normal(D)).astype(np.float32)
+        layers.append(O.Layer(mat(D, D), mat(D, D), mat(D, D), mat(D, D), mat(D, F), mat(F, D),
+                              g, np.zeros(D, np.float32), g.copy(), np.zeros(D, np.float32)))
+    model = O.Model(spec, layers, np.zeros(0, np.int64), skewed=True)
+    kc = int(np.ceil(0.3 * d))
+    kv = [[(rng.standard_normal((prompt, d), dtype=np.float32),
+            rng.standard_normal((prompt, d), dtype=np.float32)) for _ in range(H)] for _ in range(Lt)]
+    cols = [[np.sort(rng.choice(d, kc, replace=False)) for _ in range(H)] for _ in range(Lt)]
+    cfg = O.RunConfig(scheme="speculative", prompt_len=prompt, gen_len=steps + warmup, batch=1)
+    sess = O.Session.from_state(model, cfg, rng.standard_normal(D, dtype=np.float32), kv, cols)
+    marks = []
+    orig = O.layernorm
+
+    def timed_ln(x, g, b, eps):  # LN1 of each layer opens a layer: a free layer clock
+        if g is sess.model.layers[len(marks) % Lt].ln1_gain:
+            marks.append(time.perf_counter())
+        return orig(x, g, b, eps)
+
+    O.layernorm = timed_ln
+    per_layer = []
+    try:
+        for i in range(steps + warmup):
+            marks.clear()
+            t0 = time.perf_counter()
+            sess.decode_step()
+            t1 = time.perf_counter()
+            if i >= warmup and len(marks) == Lt:
+                per_layer.append([marks[1] - marks[0], marks[2] - marks[1], t1 - marks[2]])
+    finally:
+        O.layernorm = orig
+    t0_, t1_, tl_ = (statistics.median(x) for x in zip(*per_layer))
+    t_seq = t0_ + (L_full - 2) * t1_ + tl_
+    import threadpoolctl
+    threads = sum(p.get("num_threads", 0) for p in threadpoolctl.threadpool_info()
+                  if p.get("user_api") == "blas") or os.cpu_count()
+    return {"value": 1.0 / t_seq, "unit": UNIT, "cores": int(threads), "kind": "port",
+            "sample": (f"oracle port (reference algorithm, NumPy/OpenBLAS) decode_step of a {Lt}-layer "
+                       f"{shape} truncation, s={prompt}, 1 sequence, {len(per_layer)} timed steps; "
+                       f"T_step = T0 + {L_full - 2}*T1 + T_last = {t_seq:.3f} s/seq, batch {batch} "
+                       f"runs serially -> {batch} tok per {batch * t_seq:.2f} s (extrapolated)"),
+            "t_layer0_s": t0_, "t_layer_mid_s": t1_, "t_layer_last_s": tl_, "t_seq_s": t_seq}
+
+
+def run_reference_arm(a) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cb = cpu_reference(a.shape, a.batch, a.prompt, steps=a.steps, warmup=min(a.warmup, 1))
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "impl": "reference",
+            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": 1000.0 * a.batch / cb["value"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": _config(a), "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _config(a) -> dict:
+    from paper_2406_19707_b200.model import SHAPES
+    sh = SHAPES[a.shape]
+    return {"workload": WORKLOAD["name"], "model": a.shape, "layers": a.layers or sh["layers"],
+            "model_dim": sh["model_dim"], "heads": sh["heads"], "ffn_dim": sh["ffn_dim"],
+            "global_batch": a.batch, "context": a.prompt, "partial_ratio": WORKLOAD["ratio"],
+            "alpha": WORKLOAD["alpha"], "cap_ratio": WORKLOAD["cap"],
+            "outlier_scale": WORKLOAD["outlier_scale"], "kv_pool": "pinned host, f16",
+            "parallelism": f"tp{a.gpus} (heads)" if a.gpus > 1 else "single GPU",
+            "l2": "inputs larger than L2 (partial K >= 1.6 GB streamed per layer set; host pool 54 GB)"}
+
+
+# --------------------------------------------------------------- B200 arm
+def run_b200(a) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2406_19707_b200 import _lib
+    from paper_2406_19707_b200.engine import DecodeEngine, RunConfig
+    from paper_2406_19707_b200.model import SHAPES, ModelSpec, generate_synthetic_gpu, skew_model_gpu
+    from paper_2406_19707_b200.speculation import SpeculationConfig
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    sh = dict(SHAPES[a.shape])
+    if a.layers:
+        sh["layers"] = a.layers
+    spec = ModelSpec(**sh, outlier_channels=8, outlier_scale=WORKLOAD["outlier_scale"], seed=0)
+    t_setup = time.time()
+    model = generate_synthetic_gpu(spec, device=dev)
+    skew_model_gpu(model)
+    steps_total = a.warmup + 2 * a.steps + 4
+    cfg = RunConfig(scheme="speculative", prompt_len=a.prompt, gen_len=steps_total, batch=a.batch,
+                    speculation=SpeculationConfig(WORKLOAD["ratio"], WORKLOAD["alpha"], WORKLOAD["cap"], 1))
+    eng = DecodeEngine(model, cfg, pool_dtype="f16", device=dev, group=group, fetch_ctas=a.fetch_ctas)
+    # engine holds its own (sharded) copies: drop the full model
+    del model
+    torch.cuda.empty_cache()
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234)
+    prompts = torch.empty(a.batch, a.prompt, spec.model_dim, device=dev).normal_(generator=g)
+    eng.prefill(prompts, tf32=True)
+    del prompts
+    torch.cuda.empty_cache()
+    setup_s = time.time() - t_setup
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(a.warmup):
+        eng.decode_step()
+    barrier()
+    # -------- device-timed region: K steps, inputs resident in HBM / host pool
+    launches0 = _lib.launches
+    eng.instrument(a.steps)
+    cur = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(cur)
+        for _ in range(a.steps):
+            eng.decode_step()
+        e1.record(cur)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    launches = _lib.launches - launches0
+    stats = eng.kernel_stats()
+    eng._inst = None
+    # -------- end-to-end: public API with host input/output rows each step
+    x_host = torch.empty((a.batch, spec.model_dim), dtype=torch.float32).pin_memory()
+    x_host.copy_(eng.x.cpu())
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        out = eng.step_host(x_host.numpy())
+        x_host.copy_(torch.from_numpy(out))
+    barrier()
+    e2e_ms = (time.perf_counter() - t0) * 1000.0
+    ms_t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms, e2e_ms = float(ms_t[0]), float(ms_t[1])
+
+    if rank == 0:
+        tok = a.batch * a.steps
+        value = tok / (ms / 1000.0)
+        hbm_peak = _peak("hbm_gbs", 6452.8)
+        link_peak = _link_peak(dev)
+        fetch_keys = [k for k in ("fetch_gather", "fetch_all_ce") if k in stats]
+        f_bytes = sum(stats[k]["bytes"] for k in fetch_keys)
+        f_ms = sum(stats[k]["ms"] for k in fetch_keys)
+        f_launch = sum(stats[k]["launches"] for k in fetch_keys)
+        fetch_gbs = f_bytes / (f_ms * 1e6) if f_ms else None
+        roof = {"kernel": "fetch (ig_fetch zero-copy gather + ig_fetch_all copy-engine rows)",
+                "bound": "host_link", "achieved": fetch_gbs, "peak": link_peak["gbs"],
+                "peak_source": link_peak["source"], "unit": "GB/s",
+                "frac": (fetch_gbs / link_peak["gbs"]) if fetch_gbs else None, "traffic": None,
+                "bytes_per_launch": f_bytes / max(f_launch, 1),
+                "step_share": f_ms / ms if ms else None}
+        hbm = {}
+        for k in ("rehearse", "attend", "select"):
+            if k in stats:
+                gbs = stats[k]["gbs"]
+                hbm[k] = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                          "frac": gbs / hbm_peak if gbs else None,
+                          "bytes_per_launch": stats[k]["bytes"] / stats[k]["launches"],
+                          "ms_per_launch": stats[k]["ms"] / stats[k]["launches"]}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32 compute (rehearsal, attention, dense), f16 host KV pool",
+                "data": ("synthetic: random-init OPT-13B-shaped weights (reference recipe, torch RNG), "
+                         "GPU-SVD skew, N(0,1) prompts, GPU prefill"),
+                "config": _config(a), "roofline": roof, "roofline_hbm": hbm,
+                "kernel_stats": stats, "clocks": clk.summary(),
+                "e2e": {"value": tok / (e2e_ms / 1000.0), "unit": UNIT,
+                        "h2d_bytes_per_step": a.batch * spec.model_dim * 4,
+                        "d2h_bytes_per_step": a.batch * spec.model_dim * 4},
+                "gpu_launches": launches, "setup_s": setup_s}
+        if not a.no_cpu_baseline and world == 1:
+            try:
+                line["cpu_baseline"] = cpu_reference(a.shape, a.batch, a.prompt, a.cpu_sample_steps)
+            except Exception as e:  # reported, never fatal to the GPU number
+                line["cpu_baseline"] = {"error": repr(e)}
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _peak(key, fallback):
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)[key])
+    except (OSError, KeyError, ValueError):
+        return fallback
+
+
+def _link_peak(dev) -> dict:
+    """Host link peak measured live: copy-engine H2D of 1 GiB pinned (best of 5)."""
+    import torch
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d.copy_(h, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = max(best, n / (e0.elapsed_time(e1) * 1e6))
+    return {"gbs": best, "source": "measured live: copy-engine H2D, 1 GiB pinned, best of 5"}
+
+
+def main():
+    a = _args()
+    if a.impl == "reference":
+        run_reference_arm(a)
+    else:
+        run_b200(a)
+
+
+if __name__ == "__main__":
+    main()

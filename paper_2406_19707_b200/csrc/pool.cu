@@ -100,19 +100,24 @@ __device__ void touch_rows(const int32_t* __restrict__ sel, int n, int extra, in
   __syncthreads();
   if (tid == 0) *sh_flag = 0;
   __syncthreads();
+  // Saturation is decided on the pre-increment value: ptxas (12.9, sm_100a)
+  // lowers `c = min(old + 1, 255); hit = c == 255` to a packed VIMNMX.U16x2
+  // whose second predicate output clobbers the first, making `hit` always 1.
   int hit = 0;
   for (int r = tid; r < n; r += blockDim.x) {
     const int t = sel ? sel[r] : r;
     lf[t] = fseq;
-    const int c = min((int)ctr[t] + 1, 255);
-    ctr[t] = (uint8_t)c;
-    hit |= c == 255;
+    const unsigned old = ctr[t];
+    const bool sat = old >= 254u;
+    ctr[t] = sat ? (uint8_t)255 : (uint8_t)(old + 1u);
+    hit |= (int)sat;
   }
   if (!extra_in && tid == 0) {
     lf[extra] = fseq;
-    const int c = min((int)ctr[extra] + 1, 255);
-    ctr[extra] = (uint8_t)c;
-    hit |= c == 255;
+    const unsigned old = ctr[extra];
+    const bool sat = old >= 254u;
+    ctr[extra] = sat ? (uint8_t)255 : (uint8_t)(old + 1u);
+    hit |= (int)sat;
   }
   if (hit) atomicOr(sh_flag, 1);
   __syncthreads();

@@ -189,6 +189,7 @@ class DecodeEngine:
         self._load_weights(model)
         self._alloc()
         self.s_host = 0
+        self._inst = None
         self.iteration = 0
         self.records: list = []       # per iteration: [B][L] record dicts
         self.prefill_info: dict = {}
@@ -411,11 +412,68 @@ class DecodeEngine:
                              "pool_overwrites": ovw * L * self.H}
         torch.cuda.synchronize(self.device)
 
+    # -------------------------------------------------------- instrumentation
+    def instrument(self, steps: int) -> None:
+        """Record CUDA events around every fetch / rehearse / select / attend
+        launch (on the stream it runs on) for the next ``steps`` decode steps,
+        plus the per-step n; read back with kernel_stats().  Event records
+        are asynchronous: no host synchronisation is added."""
+        self._inst = {"steps": steps, "k": 0, "ev": [], "s": [],
+                      "n": torch.zeros((steps, self.L, self.B), dtype=torch.int32, device=self.device)}
+
+    def _mark(self, kind: str, li: int, stream, start: bool):
+        inst = self._inst
+        if inst is None or inst["k"] >= inst["steps"]:
+            return
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        if start:
+            inst["ev"].append([inst["k"], kind, li, ev, None])
+        else:
+            for rec in reversed(inst["ev"]):
+                if rec[1] == kind and rec[2] == li and rec[4] is None:
+                    rec[4] = ev
+                    break
+
+    def kernel_stats(self) -> dict:
+        """Per kernel kind: launches, total ms, algorithmic bytes (see DESIGN.md
+        "Algorithmic bytes")."""
+        inst = self._inst
+        torch.cuda.synchronize(self.device)
+        n_hist = inst["n"].cpu().numpy()
+        B, Hg, d, kc, rb = self.B, self.Hg, self.d, self.kcols, self.row_bytes
+        out = {}
+        for k, kind, li, e0, e1 in inst["ev"]:
+            if e1 is None:
+                continue
+            s = inst["s"][k]
+            if kind == "fetch":
+                rows = B * s if (li == 0 or self.scheme == "full") else int(n_hist[k, li].sum())
+                nbytes = rows * Hg * rb
+            elif kind == "rehearse":
+                nbytes = 4 * B * Hg * s * (kc + 1)            # partial K read + scores write
+            elif kind == "select":
+                nbytes = 4 * B * Hg * s                       # one pass over the scores
+            else:                                             # attend: staged rows read
+                rows = B * s if (li == 0 or self.scheme == "full") else int(n_hist[k, li].sum())
+                nbytes = rows * Hg * rb
+            tag = kind if kind != "fetch" else ("fetch_all_ce" if (li == 0 or self.scheme == "full") else "fetch_gather")
+            r = out.setdefault(tag, {"launches": 0, "ms": 0.0, "bytes": 0})
+            r["launches"] += 1
+            r["ms"] += e0.elapsed_time(e1)
+            r["bytes"] += nbytes
+        for r in out.values():
+            r["gbs"] = r["bytes"] / (r["ms"] * 1e6) if r["ms"] > 0 else None
+        out["n_mean_per_layer"] = [float(x) for x in n_hist[:inst["k"]].mean(axis=(0, 2))]
+        return out
+
     # ----------------------------------------------------------------- decode
     def _issue_full_fetch(self, li: int, s: int, stage: torch.Tensor) -> None:
+        self._mark("fetch", li, self.fetch_stream, True)
         _lib.call("ig_fetch_all", self._pool_layer_host(li), self.B, self.Hg, self.S_max, s,
                   self.row_bytes, stage.data_ptr(), self.S_max,
                   self.fetch_stream.cuda_stream, kernels=0)
+        self._mark("fetch", li, self.fetch_stream, False)
 
     def _attend(self, li: int, stage, idx, n, stage_rows: int, cs: int) -> None:
         Hgd = self.Hg * self.d
@@ -461,11 +519,14 @@ class DecodeEngine:
                 if nxt < L:
                     if speculative:
                         torch.matmul(self.x_a, self.wqkv[nxt][:, :Hgd], out=self.qspec)
+                        self._mark("rehearse", nxt, C, True)
                         _lib.call("ig_rehearse", self.qspec.data_ptr(), Hgd,
                                   self.cols[nxt].data_ptr(), self.pk[nxt - 1].data_ptr(),
                                   self.st.data_ptr(), B, Hg, d, self.kcols, self.S_max,
                                   self.scale, self.scores.data_ptr(),
                                   self.maxkey[nxt].data_ptr(), cs)
+                        self._mark("rehearse", nxt, C, False)
+                        self._mark("select", nxt, C, True)
                         _lib.call("ig_count", self.scores.data_ptr(), self.maxkey[nxt].data_ptr(),
                                   self.st.data_ptr(), B, Hg, self.S_max, float(sc.alpha),
                                   self.counts.data_ptr(), self.count_sum[nxt].data_ptr(), cs)
@@ -476,14 +537,17 @@ class DecodeEngine:
                                   self.H, self.S_max, self.cap, float(sc.cap_ratio),
                                   int(sc.min_select), self.idx[nxt].data_ptr(),
                                   self.n[nxt].data_ptr(), self.err.data_ptr(), cs)
+                        self._mark("select", nxt, C, False)
                         if cfg.record_scores:
                             spec_scores[nxt] = self.scores[:, :, :s].cpu()
                         self.ev_sel[nxt].record(C)
                         Fs.wait_event(self.ev_sel[nxt])
+                        self._mark("fetch", nxt, Fs, True)
                         _lib.call("ig_fetch", self._pool_layer_dev(nxt), self.idx[nxt].data_ptr(),
                                   self.n[nxt].data_ptr(), B, Hg, self.S_max, self.cap,
                                   self.row_bytes, self.stage_sel[nxt % 2].data_ptr(),
                                   self.fetch_ctas, Fs.cuda_stream)
+                        self._mark("fetch", nxt, Fs, False)
                     else:
                         if li >= 1:
                             Fs.wait_event(self.ev_att[li - 1])
@@ -504,11 +568,13 @@ class DecodeEngine:
                           self.st.data_ptr(), B, Hg, d, self.S_max, self.pos[li].data_ptr(),
                           self.events[li].data_ptr(), cs)
                 C.wait_event(self.ev_fetch[li])
+                self._mark("attend", li, C, True)
                 if sel:
                     self._attend(li, self.stage_sel[li % 2], self.idx[li], self.n[li], self.cap, cs)
                 else:
                     stage = self.stage_full[0] if speculative else self.stage_full[li % 2]
                     self._attend(li, stage, None, None, self.S_max, cs)
+                self._mark("attend", li, C, False)
                 self.ev_att[li].record(C)
                 torch.matmul(self.attn, self.wo[li], out=self.o)
                 if self.world > 1:
@@ -524,6 +590,11 @@ class DecodeEngine:
                     self._record(li, s, recs, spec_scores)
                 x = x_new
             _lib.call("ig_step_advance", self.st.data_ptr(), cs)
+            inst = self._inst
+            if inst is not None and inst["k"] < inst["steps"]:
+                inst["n"][inst["k"]].copy_(self.n)
+                inst["s"].append(s)
+                inst["k"] += 1
             s_next = min(s + 1, cfg.pool_limit) if cfg.pool_limit else s + 1
             # next step's layer-0 rows stream in while the tail of this step runs
             # (after the last attend that reads stage_full[0])
