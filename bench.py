@@ -248,13 +248,18 @@ def run_b200(a) -> None:
     eng.instrument(a.steps)
     cur = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prof = os.environ.get("IG_PROFILE_WINDOW") == "1"   # ncu --profile-from-start off
     with ClockSampler(local) as clk:
         barrier()
+        if prof:
+            torch.cuda.profiler.start()
         e0.record(cur)
         for _ in range(a.steps):
             eng.decode_step()
         e1.record(cur)
         barrier()
+        if prof:
+            torch.cuda.profiler.stop()
     ms = e0.elapsed_time(e1)
     launches = _lib.launches - launches0
     stats = eng.kernel_stats()

@@ -171,12 +171,171 @@ attend_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_
   if (threadIdx.x == 0) tickets[bh] = 0;
 }
 
+// Fast path for 512-B rows (d = 128, 2-byte elements): one 16-B vector per
+// lane moves a whole K+V row per warp instruction -- lanes 0-15 hold 8 K
+// elements each, lanes 16-31 hold 8 V elements; the q.k partials reduce over
+// the 16 K lanes and the score is broadcast.  kFastRows rows are in flight per
+// warp.  Same online softmax, same chunk / ticket merge as attend_kernel.
+constexpr int kFastRows = 8;
+constexpr int kFastChunk = 256;
+
+template <typename T>
+__device__ __forceinline__ void unpack8(const uint4& u, float* f) {
+  const T* h = reinterpret_cast<const T*>(&u);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = Elt<T>::to_f(h[i]);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kAttThreads)
+attend512_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_cur,
+                 const float* __restrict__ v_cur, int ldkv, const T* __restrict__ stage,
+                 const int32_t* __restrict__ idx, const int32_t* __restrict__ n_in,
+                 const int32_t* __restrict__ pos_in, const ig_step_state* __restrict__ st, int Hg,
+                 int cap, float sqrt_d, int max_chunks, float* __restrict__ partial,
+                 int32_t* __restrict__ tickets, float* __restrict__ out, int ldo) {
+  constexpr int d = 128;
+  const int b = blockIdx.z, h = blockIdx.y, c = blockIdx.x;
+  const size_t bh = (size_t)b * Hg + h;
+  const int rows = n_in ? n_in[b] : st->s_len;
+  const int nchunks = max(1, (rows + kFastChunk - 1) / kFastChunk);
+  if (c >= nchunks) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool klane = lane < 16;
+  const int e0 = (lane & 15) * 8;       // first of my 8 elements (K or V)
+  const int pos = pos_in[bh];
+
+  float qv[8];
+  {
+    const float* qr = q + (size_t)b * ldq + (size_t)h * d + e0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) qv[i] = klane ? qr[i] : 0.f;
+  }
+  float m = -INFINITY, l = 0.f, acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+
+  auto consume = [&](float dot, const float* vv) {
+    // dot: per-lane partial (K lanes) -> full q.k in every lane
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    const float sc = __shfl_sync(0xffffffffu, dot, 0) / sqrt_d;
+    const float mn = fmaxf(m, sc);
+    const float corr = expf(m - mn);
+    const float p = expf(sc - mn);
+    l = l * corr + p;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = fmaf(p, vv[i], acc[i] * corr);
+    m = mn;
+  };
+
+  const int r0 = c * kFastChunk, r1 = min(rows, r0 + kFastChunk);
+  const uint4* base = reinterpret_cast<const uint4*>(stage + bh * (size_t)cap * 2 * d);
+  for (int rb = r0 + w * kFastRows; rb < r1; rb += kAttWarps * kFastRows) {
+    uint4 raw[kFastRows];
+    int rowid = 0;
+    if (idx && lane < kFastRows && rb + lane < r1) rowid = idx[bh * cap + rb + lane];
+#pragma unroll
+    for (int u = 0; u < kFastRows; ++u) {
+      const int r = rb + u;
+      if (r < r1) {
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(raw[u].x), "=r"(raw[u].y), "=r"(raw[u].z), "=r"(raw[u].w)
+                     : "l"(base + (size_t)r * 32 + lane));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kFastRows; ++u) {
+      const int r = rb + u;
+      const int id = idx ? __shfl_sync(0xffffffffu, rowid, u) : r;
+      if (r >= r1 || id == pos) continue;   // warp-uniform
+      float f[8];
+      unpack8<T>(raw[u], f);
+      float dot = 0.f;
+      if (klane) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dot = fmaf(qv[i], f[i], dot);
+      }
+      consume(dot, f);
+    }
+  }
+  if (c == 0 && w == 0) {  // the current token: GPU-resident f32 row
+    const float* src = (klane ? k_cur : v_cur) + (size_t)b * ldkv + (size_t)h * d + e0;
+    float f[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = src[i];
+    float dot = 0.f;
+    if (klane) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dot = fmaf(qv[i], f[i], dot);
+    }
+    consume(dot, f);
+  }
+
+  __shared__ float wm[kAttWarps], wl[kAttWarps];
+  __shared__ float wacc[kAttWarps][d];
+  if (lane == 0) { wm[w] = m; wl[w] = l; }
+  if (!klane) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) wacc[w][e0 + i] = acc[i];
+  }
+  __syncthreads();
+  float M = -INFINITY;
+  for (int i = 0; i < kAttWarps; ++i) M = fmaxf(M, wm[i]);
+  float* part = partial + (bh * max_chunks + c) * (size_t)(d + 2);
+  if (threadIdx.x == 0) {
+    float L = 0.f;
+    for (int i = 0; i < kAttWarps; ++i) L += wl[i] * (wm[i] == -INFINITY ? 0.f : expf(wm[i] - M));
+    part[0] = M;
+    part[1] = L;
+  }
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    float a = 0.f;
+    for (int i = 0; i < kAttWarps; ++i) a += wacc[i][e] * (wm[i] == -INFINITY ? 0.f : expf(wm[i] - M));
+    part[2 + e] = a;
+  }
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(tickets + bh, 1) == nchunks - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const float* pb = partial + bh * max_chunks * (size_t)(d + 2);
+  float MM = -INFINITY;
+  for (int i = 0; i < nchunks; ++i) MM = fmaxf(MM, __ldcg(pb + (size_t)i * (d + 2)));
+  float LL = 0.f;
+  for (int i = 0; i < nchunks; ++i) {
+    const float mi = __ldcg(pb + (size_t)i * (d + 2));
+    LL += __ldcg(pb + (size_t)i * (d + 2) + 1) * (mi == -INFINITY ? 0.f : expf(mi - MM));
+  }
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    float a = 0.f;
+    for (int i = 0; i < nchunks; ++i) {
+      const float mi = __ldcg(pb + (size_t)i * (d + 2));
+      a += __ldcg(pb + (size_t)i * (d + 2) + 2 + e) * (mi == -INFINITY ? 0.f : expf(mi - MM));
+    }
+    out[(size_t)b * ldo + (size_t)h * d + e] = a / LL;
+  }
+  if (threadIdx.x == 0) tickets[bh] = 0;
+}
+
 template <typename T>
 int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const float* k_cur,
                   const float* v_cur, int ldkv, const void* stage, const int32_t* idx,
                   const int32_t* n, const int32_t* pos, const ig_step_state* st, int Hg, int d,
                   int cap, float sqrt_d, int max_chunks, float* partial, int32_t* tickets,
                   float* out, int ldo) {
+  if constexpr (sizeof(T) == 2) {
+    if (d == 128) {  // 512-B rows: the production shape
+      const int mc = (cap + kFastChunk - 1) / kFastChunk;
+      attend512_kernel<T><<<dim3(mc, grid.y, grid.z), kAttThreads, 0, s>>>(
+          q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, pos, st, Hg, cap, sqrt_d,
+          max_chunks, partial, tickets, out, ldo);
+      IG_LAUNCH_STATUS();
+      return IG_OK;
+    }
+  }
 #define IG_ATT(E)                                                                              \
   attend_kernel<T, E><<<grid, kAttThreads, 0, s>>>(q, ldq, k_cur, v_cur, ldkv,                \
       (const T*)stage, idx, n, pos, st, Hg, d, cap, 0.f, sqrt_d, max_chunks, partial, tickets, \

@@ -15,6 +15,7 @@ namespace ig {
 
 constexpr int kSelThreads = 512;
 constexpr int kSelWarps = kSelThreads / kWarp;
+constexpr size_t kSelMaxSmem = 220 * 1024;  // keys of rows up to 56K tokens
 
 struct SelShared {
   uint32_t hist[256];
@@ -24,15 +25,48 @@ struct SelShared {
   int need;
 };
 
-// Top-n rows of `row[0:s)`, ascending, into out[0:n).  Whole block calls.
+// Choose the radix digit: bins are scanned from 255 down; the digit is the
+// bin where the running count of larger bins first reaches `need`.  One warp,
+// 8 bins per lane, warp prefix sum over lane totals (replaces a 256-step
+// serial scan).  Writes sh.prefix / sh.need.
+__device__ __forceinline__ void pick_digit(SelShared& sh, uint32_t prefix, int need, int shift) {
+  const int lane = threadIdx.x & 31;
+  // lane L owns bins 255-8L .. 248-8L (descending)
+  int c[8], tot = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { c[i] = (int)sh.hist[255 - 8 * lane - i]; tot += c[i]; }
+  int incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int excl = incl - tot;  // count in bins above my range
+  const unsigned hitmask = __ballot_sync(0xffffffffu, excl < need && incl >= need);
+  const int src = __ffs(hitmask) - 1;
+  if (lane == src) {
+    int cum = excl, bin = 255 - 8 * lane;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (cum + c[i] >= need) { bin = 255 - 8 * lane - i; break; }
+      cum += c[i];
+    }
+    sh.prefix = prefix | ((uint32_t)bin << shift);
+    sh.need = need - cum;
+  }
+}
+
+// Top-n rows of a score row, ascending, into out[0:n).  Whole block calls.
+// `keys` is this block's shared buffer of s order keys (filled here).
 __device__ void radix_topn(const float* __restrict__ row, int s, int n, int32_t* __restrict__ out,
-                           SelShared& sh) {
+                           SelShared& sh, uint32_t* __restrict__ keys) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (n >= s) {
     for (int t = tid; t < s; t += blockDim.x) out[t] = t;
     return;
   }
   if (n <= 0) return;
+  for (int t = tid; t < s; t += blockDim.x) keys[t] = order_key(row[t]);
   uint32_t prefix = 0, mask = 0;
   int need = n;
   for (int pass = 0; pass < 4; ++pass) {
@@ -44,7 +78,7 @@ __device__ void radix_topn(const float* __restrict__ row, int s, int n, int32_t*
       bool live = false;
       uint32_t bin = 0;
       if (t < s) {
-        const uint32_t key = order_key(row[t]);
+        const uint32_t key = keys[t];
         live = (key & mask) == prefix;
         bin = (key >> shift) & 255u;
       }
@@ -56,29 +90,18 @@ __device__ void radix_topn(const float* __restrict__ row, int s, int n, int32_t*
       }
     }
     __syncthreads();
-    if (tid == 0) {
-      int cum = 0, digit = 0;
-      for (int bin = 255; bin >= 0; --bin) {
-        const int c = (int)sh.hist[bin];
-        if (cum + c >= need) { digit = bin; break; }
-        cum += c;
-      }
-      sh.prefix = prefix | ((uint32_t)digit << shift);
-      sh.need = need - cum;
-    }
+    if (w == 0) pick_digit(sh, prefix, need, shift);
     __syncthreads();
     prefix = sh.prefix;
     need = sh.need;
     mask |= 255u << shift;
-    __syncthreads();
   }
   const uint32_t pivot = prefix;  // the n-th largest key; take `need` of its ties
   const unsigned lt_mask = (1u << lane) - 1u;
   int eq_base = 0, out_base = 0;
   for (int t0 = 0; t0 < s && out_base < n; t0 += blockDim.x) {
     const int t = t0 + tid;
-    uint32_t key = 0;
-    if (t < s) key = order_key(row[t]);
+    const uint32_t key = t < s ? keys[t] : 0u;
     const bool gt = t < s && key > pivot;
     const bool eq = t < s && key == pivot;
     const unsigned eqb = __ballot_sync(0xffffffffu, eq);
@@ -115,6 +138,7 @@ select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ coun
               double cap_ratio, int min_select, int32_t* __restrict__ idx,
               int32_t* __restrict__ n_out, int32_t* __restrict__ err_flag) {
   __shared__ SelShared sh;
+  extern __shared__ uint32_t keys[];
   const int b = blockIdx.y, h = blockIdx.x;
   const int s = st->s_len;
   // n = floor(sum/H + 0.5) == floor((2 sum + H) / 2H) exactly (integers)
@@ -130,7 +154,7 @@ select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ coun
   }
   if (h == 0 && threadIdx.x == 0) n_out[b] = nn;
   const size_t bh = (size_t)b * Hg + h;
-  radix_topn(scores + bh * S_max, s, nn, idx + bh * cap_max, sh);
+  radix_topn(scores + bh * S_max, s, nn, idx + bh * cap_max, sh, keys);
 }
 
 // Rewrite idx[0:n) of each (b, h) into stable descending-score order
@@ -165,7 +189,8 @@ __global__ void order_kernel(const float* __restrict__ scores, const int32_t* __
 __global__ void __launch_bounds__(kSelThreads)
 topk_rows_kernel(const float* __restrict__ values, int len, int k, int32_t* __restrict__ out) {
   __shared__ SelShared sh;
-  radix_topn(values + (size_t)blockIdx.x * len, len, k, out + (size_t)blockIdx.x * k, sh);
+  extern __shared__ uint32_t keys[];
+  radix_topn(values + (size_t)blockIdx.x * len, len, k, out + (size_t)blockIdx.x * k, sh, keys);
 }
 
 }  // namespace ig
@@ -179,7 +204,12 @@ extern "C" int ig_select(const float* scores, const int32_t* count_sum, const ig
       cap_ratio > 1 || min_select < 1 || !scores || !count_sum || !st || !idx || !n_out ||
       !err_flag)
     return IG_EINVAL;
-  select_kernel<<<dim3(Hg, B), kSelThreads, 0, (cudaStream_t)stream>>>(
+  const size_t smem = (size_t)S_max * 4;  // the row's order keys
+  if (smem > kSelMaxSmem) return IG_EINVAL;
+  if (smem > 48 * 1024)
+    IG_CUDA_STATUS(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+  select_kernel<<<dim3(Hg, B), kSelThreads, smem, (cudaStream_t)stream>>>(
       scores, count_sum, st, Hg, H_total, S_max, cap_max, cap_ratio, min_select, idx, n_out,
       err_flag);
   IG_LAUNCH_STATUS();
@@ -205,7 +235,12 @@ extern "C" int ig_topk_rows(const float* values, int rows, int len, int k, int32
   using namespace ig;
   if (rows < 1 || len < 1 || k < 0 || k > len || !values || !idx_out) return IG_EINVAL;
   if (k == 0) return IG_OK;
-  topk_rows_kernel<<<rows, kSelThreads, 0, (cudaStream_t)stream>>>(values, len, k, idx_out);
+  const size_t smem = (size_t)len * 4;
+  if (smem > kSelMaxSmem) return IG_EINVAL;
+  if (smem > 48 * 1024)
+    IG_CUDA_STATUS(cudaFuncSetAttribute(topk_rows_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  topk_rows_kernel<<<rows, kSelThreads, smem, (cudaStream_t)stream>>>(values, len, k, idx_out);
   IG_LAUNCH_STATUS();
   return IG_OK;
 }

@@ -18,7 +18,7 @@ are in HOW, not WHAT:
     pools and partial keys; per layer it all-reduces the B head-count sums
     (n averages over ALL heads, speculation.py:154-158) and the W_O output.
 
-Hot ops are the library kernels (ig_rehearse, ig_count, ig_select, ig_fetch,
+Hot ops are the library kernels (ig_rehearse_count, ig_select, ig_fetch,
 ig_fetch_all, ig_append, ig_attend, ig_layernorm); the dense projections
 are plain fp32 cuBLAS GEMMs with TF32 off.  No CPU fallback exists.
 """
@@ -148,10 +148,15 @@ class DecodeEngine:
     pool_dtype : "f16" (default, e = 2 bytes), "bf16" or "f32"
     group : torch.distributed process group for head tensor parallelism
     fetch_ctas : CTAs of the zero-copy gather (the rest of the GPU computes)
+    hbm_layers : 0 (default: every layer's KV in the pinned host pool) or 1:
+        keep layer 0's rows -- which every step reads in full (engine.py:393-396)
+        -- resident in HBM, so they never cross the host link.  Traces keep the
+        reference byte accounting; bench.py reports moved bytes separately.
     """
 
     def __init__(self, model, config: RunConfig, *, max_steps: int | None = None,
-                 pool_dtype: str = "f16", device=None, group=None, fetch_ctas: int = 32):
+                 pool_dtype: str = "f16", device=None, group=None, fetch_ctas: int = 32,
+                 hbm_layers: int = 0):
         config.validate()
         _lib.load()
         _enable_ieee_fp32()
@@ -185,6 +190,9 @@ class DecodeEngine:
         self.cap = max(int(math.floor(sc.cap_ratio * self.S_max)), sc.min_select, 1)
         self.policy = EvictionPolicy(config.pool_policy)
         self.fetch_ctas = fetch_ctas
+        if hbm_layers not in (0, 1) or hbm_layers > spec.layers:
+            raise ValueError("hbm_layers must be 0 or 1")
+        self.hbm_layers = hbm_layers
         self.scale = float(np.float32(1.0 / np.sqrt(d)))   # speculation.py:127
         self._load_weights(model)
         self._alloc()
@@ -213,9 +221,12 @@ class DecodeEngine:
         dev, B, L, Hg, d, S, cap = self.device, self.B, self.L, self.Hg, self.d, self.S_max, self.cap
         D, F, kc = self.D, self.F, self.kcols
         i32, i64, f32 = torch.int32, torch.int64, torch.float32
-        pool_bytes = L * B * Hg * S * self.row_bytes
-        self.pool = HostPool(pool_bytes)
         self.layer_bytes = B * Hg * S * self.row_bytes
+        host_layers = max(L - self.hbm_layers, 1)
+        self.pool = HostPool(host_layers * self.layer_bytes)
+        T = _TORCH_ELT[self.elt]
+        self.pool_hbm = (torch.zeros((self.hbm_layers, B, Hg, S, 2 * d), dtype=T, device=dev)
+                         if self.hbm_layers else None)
         spec_ = self.scheme == "speculative"
         self.pk = torch.zeros((max(L - 1, 1), B, Hg, kc, S), dtype=f32, device=dev) if spec_ else None
         self.cols = torch.zeros((L, B, Hg, kc), dtype=i32, device=dev)
@@ -241,9 +252,9 @@ class DecodeEngine:
         self.err = torch.zeros(1, dtype=i32, device=dev)
         self.pos = torch.zeros((L, B, Hg), dtype=i32, device=dev)
         self.events = torch.zeros((L, B, Hg, 2), dtype=i64, device=dev)
-        T = _TORCH_ELT[self.elt]
+        n_full = (0 if self.hbm_layers else 1) if spec_ else 2
         self.stage_full = [torch.empty((B, Hg, S, 2 * d), dtype=T, device=dev)
-                           for _ in range(1 if spec_ else 2)]
+                           for _ in range(n_full)]
         self.stage_sel = [torch.empty((B, Hg, cap, 2 * d), dtype=T, device=dev)
                           for _ in range(2 if spec_ else 0)]
         pf, tk = ctypes.c_size_t(), ctypes.c_size_t()
@@ -266,15 +277,29 @@ class DecodeEngine:
         self.s_host = s_len
 
     def pool_view(self) -> np.ndarray:
-        """Host pool as [L][B][Hg][S_max][2][d] (no copy)."""
+        """Host pool as [L - hbm_layers][B][Hg][S_max][2][d] (no copy)."""
         npdt = {"f32": np.float32, "f16": np.float16, "bf16": np.uint16}[self.elt]
-        return self.pool.numpy(npdt, (self.L, self.B, self.Hg, self.S_max, 2, self.d))
+        return self.pool.numpy(npdt, (max(self.L - self.hbm_layers, 1), self.B, self.Hg,
+                                      self.S_max, 2, self.d))
+
+    def layer_rows(self, li: int) -> np.ndarray:
+        """Layer li's pool rows [B][Hg][S_max][2][d] as a host array (copy)."""
+        if li < self.hbm_layers:
+            t = self.pool_hbm[li].view(self.B, self.Hg, self.S_max, 2, self.d)
+            return (t.view(torch.uint16) if self.elt == "bf16" else t).cpu().numpy()
+        return np.array(self.pool_view()[li - self.hbm_layers])
 
     def _pool_layer_dev(self, li: int) -> int:
-        return self.pool.dev + li * self.layer_bytes
+        """Device address of layer li's rows (HBM tier or the host pool alias)."""
+        if li < self.hbm_layers:
+            return self.pool_hbm[li].data_ptr()
+        return self.pool.dev + (li - self.hbm_layers) * self.layer_bytes
 
     def _pool_layer_host(self, li: int) -> int:
-        return self.pool.host + li * self.layer_bytes
+        """Copy-engine address of layer li's rows (UVA: host pointer or HBM)."""
+        if li < self.hbm_layers:
+            return self.pool_hbm[li].data_ptr()
+        return self.pool.host + (li - self.hbm_layers) * self.layer_bytes
 
     # ---------------------------------------------------------- state import
     def load_state(self, x, kv, columns=None, meta=None) -> None:
@@ -301,12 +326,17 @@ class DecodeEngine:
                         s_len = s
                     if s != s_len or s > S:
                         raise ValueError("all pools must hold the same row count <= S_max")
-                    if self.elt == "bf16":
+                    if li < self.hbm_layers:
+                        rows = torch.from_numpy(np.concatenate([K, V], axis=1)).to(self.device)
+                        self.pool_hbm[li, b, hl, :s] = rows.to(self.pool_hbm.dtype)
+                    elif self.elt == "bf16":
                         kb = torch.from_numpy(K).to(torch.bfloat16).view(torch.uint16).numpy()
                         vb = torch.from_numpy(V).to(torch.bfloat16).view(torch.uint16).numpy()
-                        pv[li, b, hl, :s, 0], pv[li, b, hl, :s, 1] = kb, vb
+                        lh = li - self.hbm_layers
+                        pv[lh, b, hl, :s, 0], pv[lh, b, hl, :s, 1] = kb, vb
                     else:
-                        pv[li, b, hl, :s, 0], pv[li, b, hl, :s, 1] = K, V
+                        lh = li - self.hbm_layers
+                        pv[lh, b, hl, :s, 0], pv[lh, b, hl, :s, 1] = K, V
                     if meta is not None and meta(li, b, h) is not None:
                         a_, l_, c_, sq = meta(li, b, h)
                         arr[li, b, hl, :s], lf[li, b, hl, :s], ct[li, b, hl, :s] = a_, l_, c_
@@ -503,10 +533,11 @@ class DecodeEngine:
         spec_scores = [None] * L
         C.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(C):
-            self.maxkey.zero_()
             self.count_sum.zero_()
             self.ev_step.record(C)
-            if not self._prefetched0:
+            if self.hbm_layers:
+                self.ev_fetch[0].record(C)          # layer 0 is HBM-resident: no fetch
+            elif not self._prefetched0:
                 Fs.wait_event(self.ev_step)
                 self._issue_full_fetch(0, s, self.stage_full[0])
                 self.ev_fetch[0].record(Fs)
@@ -520,16 +551,13 @@ class DecodeEngine:
                     if speculative:
                         torch.matmul(self.x_a, self.wqkv[nxt][:, :Hgd], out=self.qspec)
                         self._mark("rehearse", nxt, C, True)
-                        _lib.call("ig_rehearse", self.qspec.data_ptr(), Hgd,
+                        _lib.call("ig_rehearse_count", self.qspec.data_ptr(), Hgd,
                                   self.cols[nxt].data_ptr(), self.pk[nxt - 1].data_ptr(),
                                   self.st.data_ptr(), B, Hg, d, self.kcols, self.S_max,
-                                  self.scale, self.scores.data_ptr(),
-                                  self.maxkey[nxt].data_ptr(), cs)
+                                  self.scale, float(sc.alpha), 0, self.scores.data_ptr(),
+                                  self.counts.data_ptr(), self.count_sum[nxt].data_ptr(), cs)
                         self._mark("rehearse", nxt, C, False)
                         self._mark("select", nxt, C, True)
-                        _lib.call("ig_count", self.scores.data_ptr(), self.maxkey[nxt].data_ptr(),
-                                  self.st.data_ptr(), B, Hg, self.S_max, float(sc.alpha),
-                                  self.counts.data_ptr(), self.count_sum[nxt].data_ptr(), cs)
                         if self.world > 1:
                             dist.all_reduce(self.count_sum[nxt], group=self.group)
                         _lib.call("ig_select", self.scores.data_ptr(),
@@ -571,6 +599,8 @@ class DecodeEngine:
                 self._mark("attend", li, C, True)
                 if sel:
                     self._attend(li, self.stage_sel[li % 2], self.idx[li], self.n[li], self.cap, cs)
+                elif li < self.hbm_layers:
+                    self._attend(li, self.pool_hbm[li], None, None, self.S_max, cs)
                 else:
                     stage = self.stage_full[0] if speculative else self.stage_full[li % 2]
                     self._attend(li, stage, None, None, self.S_max, cs)
@@ -598,11 +628,12 @@ class DecodeEngine:
             s_next = min(s + 1, cfg.pool_limit) if cfg.pool_limit else s + 1
             # next step's layer-0 rows stream in while the tail of this step runs
             # (after the last attend that reads stage_full[0])
-            last0 = 0 if speculative else (L - 1 if (L - 1) % 2 == 0 else L - 2)
-            Fs.wait_event(self.ev_att[last0])
-            self._issue_full_fetch(0, s_next, self.stage_full[0])
-            self.ev_fetch[0].record(Fs)
-            self._prefetched0 = True
+            if not self.hbm_layers:
+                last0 = 0 if speculative else (L - 1 if (L - 1) % 2 == 0 else L - 2)
+                Fs.wait_event(self.ev_att[last0])
+                self._issue_full_fetch(0, s_next, self.stage_full[0])
+                self.ev_fetch[0].record(Fs)
+                self._prefetched0 = True
             self.x = x
         torch.cuda.current_stream(self.device).wait_stream(C)
         self.s_host = s_next

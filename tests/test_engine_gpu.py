@@ -116,21 +116,71 @@ def test_engine_f32_pool_matches_oracle(mname, rname):
         eng.close()
 
 
+# (pool dtype, output tolerance, min selection agreement): 2-byte K/V round the
+# attended rows (f16: 11-bit, bf16: 8-bit significand) and move x, hence later
+# selections; the bars are stated here and in DESIGN.md s2.
+TWO_BYTE = [("f16", 5e-3, 0.97), ("bf16", 3e-2, 0.93)]
+
+
+@pytest.mark.parametrize("pool,tol,agree", TWO_BYTE)
 @pytest.mark.parametrize("mname", sorted(MODELS))
-def test_engine_f16_pool_tolerance(mname):
+def test_engine_2byte_pool_tolerance(mname, pool, tol, agree):
     from paper_2406_19707_b200 import DecodeEngine
     _, sk = models(mname)
     ocfg = run_config("spec", record_selection=True)
     sessions = oracle_sessions(sk, ocfg)
-    eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg), copy.deepcopy(sessions), pool_dtype="f16")
+    eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg), copy.deepcopy(sessions), pool_dtype=pool)
     try:
         ref_out, ref_recs = oracle_decode(sessions, ocfg.gen_len)
         got = np.stack([eng.x.cpu().numpy()] + [eng.decode_step().cpu().numpy()
                                                 for _ in range(ocfg.gen_len)], axis=1)
-        assert _scaled_err(got, ref_out) < 5e-3
-        assert _cmp_records(eng.records, ref_recs, ocfg.batch, exact=False) >= 0.97
+        assert _scaled_err(got, ref_out) < tol
+        assert _cmp_records(eng.records, ref_recs, ocfg.batch, exact=False) >= agree
     finally:
         eng.close()
+
+
+def test_fast_attention_path_matches_generic():
+    """d = 128 with a 2-byte pool takes attend512_kernel; the same rows in an
+    f32 pool take the generic kernel: results agree to the f16 rounding of K/V."""
+    import torch
+    from paper_2406_19707_b200 import _lib
+    rng = np.random.default_rng(11)
+    B, Hg, d, cap = 3, 5, 128, 700
+    q = torch.from_numpy(rng.standard_normal((B, Hg * d)).astype(np.float32)).cuda()
+    kc = torch.from_numpy(rng.standard_normal((B, Hg * d)).astype(np.float32)).cuda()
+    vc = torch.from_numpy(rng.standard_normal((B, Hg * d)).astype(np.float32)).cuda()
+    rows16 = torch.from_numpy((rng.standard_normal((B, Hg, cap, 2 * d)) * 2).astype(np.float16)).cuda()
+    rows32 = rows16.float()
+    n = torch.tensor([700, 1, 333], dtype=torch.int32, device="cuda")
+    idx = torch.from_numpy(np.tile(np.arange(cap, dtype=np.int32) * 3, (B, Hg, 1))).cuda()
+    pos = torch.full((B, Hg), 9, dtype=torch.int32, device="cuda")   # row 3 (idx 9) is excluded
+    st = torch.zeros(8, dtype=torch.int32, device="cuda")
+    outs = []
+    for rows, elt in ((rows16, "f16"), (rows32, "f32")):
+        import ctypes
+        pf, tk = ctypes.c_size_t(), ctypes.c_size_t()
+        _lib.call("ig_attend_scratch", B, Hg, d, cap, ctypes.byref(pf), ctypes.byref(tk), kernels=0)
+        part = torch.empty(pf.value, dtype=torch.float32, device="cuda")
+        tick = torch.zeros(tk.value, dtype=torch.int32, device="cuda")
+        out = torch.empty((B, Hg * d), dtype=torch.float32, device="cuda")
+        _lib.call("ig_attend", q.data_ptr(), Hg * d, kc.data_ptr(), vc.data_ptr(), Hg * d,
+                  rows.data_ptr(), _lib.ELT[elt], idx.data_ptr(), n.data_ptr(), pos.data_ptr(),
+                  st.data_ptr(), B, Hg, d, cap, part.data_ptr(), tick.data_ptr(), out.data_ptr(),
+                  Hg * d, _lib.stream_handle())
+        outs.append(out.cpu().numpy())
+    np.testing.assert_allclose(outs[0], outs[1], rtol=1e-5, atol=1e-5)
+    # and against a float64 reference of the same semantics
+    r = rows32.cpu().numpy().astype(np.float64)
+    for b in range(B):
+        for h in range(Hg):
+            keep = [i for i in range(int(n[b])) if i != 3]
+            K = np.concatenate([r[b, h, keep, :d], kc.cpu().numpy()[b, h * d:(h + 1) * d][None]])
+            V = np.concatenate([r[b, h, keep, d:], vc.cpu().numpy()[b, h * d:(h + 1) * d][None]])
+            sc = K @ q.cpu().numpy()[b, h * d:(h + 1) * d].astype(np.float64) / np.sqrt(d)
+            w = np.exp(sc - sc.max())
+            ref = (w / w.sum()) @ V
+            np.testing.assert_allclose(outs[0][b, h * d:(h + 1) * d], ref, rtol=2e-4, atol=2e-4)
 
 
 def test_hook_mode_drop_in(monkeypatch):
@@ -221,3 +271,26 @@ def test_batch_rows_are_independent():
         single = engine_cfg(ocfg, batch=1, prompt_seed=b)
         _, one = run(sk, single, pool_dtype="f32")
         assert _scaled_err(outs[b], one[0]) < 1e-5
+
+
+@pytest.mark.parametrize("rname", ["spec", "spec_counter", "full"])
+def test_hbm_resident_layer0_is_identical(rname):
+    """hbm_layers=1 keeps layer 0's rows in HBM: same outputs, same records."""
+    from paper_2406_19707_b200 import DecodeEngine
+    plain, sk = models("m64")
+    ocfg = run_config(rname, record_selection=True)
+    model = sk if ocfg.scheme == "speculative" else plain
+    sessions = oracle_sessions(model, ocfg)
+    outs, recs, rows = [], [], []
+    for hbm in (0, 1):
+        eng = DecodeEngine.from_sessions(model, engine_cfg(ocfg), copy.deepcopy(sessions),
+                                         pool_dtype="f32", hbm_layers=hbm)
+        try:
+            outs.append(np.stack([eng.decode_step().cpu().numpy() for _ in range(ocfg.gen_len)]))
+            recs.append(eng.records)
+            rows.append(eng.layer_rows(0))
+        finally:
+            eng.close()
+    np.testing.assert_array_equal(outs[0], outs[1])
+    assert recs[0] == recs[1]
+    np.testing.assert_array_equal(rows[0], rows[1])   # appends / evictions land alike

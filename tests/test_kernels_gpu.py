@@ -160,3 +160,49 @@ def test_layernorm_vs_oracle():
         got = layernorm(torch.from_numpy(x).cuda(), torch.from_numpy(g).cuda(),
                         torch.from_numpy(b).cuda(), 1e-5).cpu().numpy()
         np.testing.assert_allclose(got, ref, rtol=1e-6, atol=2e-6)
+
+
+@pytest.mark.parametrize("cluster", [0, 1, 2, 3, 8])
+@pytest.mark.parametrize("s", [1, 5, 1023, 4101])
+def test_rehearse_count_fused_matches_oracle(cluster, s):
+    """ig_rehearse_count (cluster/DSMEM max + count exchange) == oracle
+    speculate_scores + the count half of select_tokens, per (b, h)."""
+    import torch
+    from paper_2406_19707_b200 import _lib
+    rng = np.random.default_rng(s * 10 + cluster)
+    B, Hg, d, k, D = 3, 4, 32, 10, 96
+    S = (s + 3) // 4 * 4
+    alpha = 2.0
+    x = rng.standard_normal((B, D)).astype(np.float32)
+    wq = rng.standard_normal((D, Hg * d)).astype(np.float32)
+    cols = np.stack([[np.sort(rng.choice(d, k, replace=False)) for _ in range(Hg)] for _ in range(B)])
+    pkey = rng.standard_normal((B, Hg, s, k)).astype(np.float32) * 2
+    qspec = (x @ wq).astype(np.float32)
+    dev = "cuda"
+    pk = torch.zeros((B, Hg, k, S), dtype=torch.float32, device=dev)
+    pk[..., :s] = torch.from_numpy(np.ascontiguousarray(pkey.transpose(0, 1, 3, 2))).to(dev)
+    scores = torch.empty((B, Hg, S), dtype=torch.float32, device=dev)
+    counts = torch.zeros((B, Hg), dtype=torch.int32, device=dev)
+    csum = torch.zeros(B, dtype=torch.int32, device=dev)
+    st = torch.zeros(8, dtype=torch.int32, device=dev)
+    st[0] = s
+    tq = torch.from_numpy(qspec).to(dev)
+    tc = torch.from_numpy(cols.astype(np.int32)).to(dev)
+    scale = float(np.float32(1.0 / np.sqrt(d)))
+    _lib.call("ig_rehearse_count", tq.data_ptr(), Hg * d, tc.data_ptr(), pk.data_ptr(), st.data_ptr(),
+              B, Hg, d, k, S, scale, alpha, cluster, scores.data_ptr(), counts.data_ptr(),
+              csum.data_ptr(), _lib.stream_handle())
+    got_s = scores.cpu().numpy()[..., :s]
+    got_c = counts.cpu().numpy()
+    for b in range(B):
+        arts = O.Partials(2, Hg)
+        for h in range(Hg):
+            arts.set_head(1, h, O.HeadPartial(cols[b, h], wq[:, h * d:(h + 1) * d][:, cols[b, h]],
+                                              pkey[b, h]))
+        ref = O.speculate_scores(x[b], arts, 1, d)
+        for h in range(Hg):
+            np.testing.assert_allclose(got_s[b, h], ref[h], rtol=1e-5, atol=1e-5)
+            # the count on the GPU's own scores must follow the reference rule exactly
+            v = got_s[b, h]
+            assert got_c[b, h] == int(np.sum(v > (float(np.max(v)) - alpha)))
+        assert int(csum[b]) == int(got_c[b].sum())
