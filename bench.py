@@ -54,6 +54,8 @@ def _args():
     ap.add_argument("--shape", default=WORKLOAD["shape"])
     ap.add_argument("--layers", type=int, default=None, help="override (debug only)")
     ap.add_argument("--fetch-ctas", type=int, default=32)
+    ap.add_argument("--no-hbm-variant", action="store_true",
+                    help="skip the secondary run with layer 0's KV resident in HBM")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=2)
     return ap.parse_args()
@@ -220,7 +222,8 @@ def run_b200(a) -> None:
     t_setup = time.time()
     model = generate_synthetic_gpu(spec, device=dev)
     skew_model_gpu(model)
-    steps_total = a.warmup + 2 * a.steps + 4
+    # warmup + timed + e2e + (HBM variant: 2 + timed) decode steps, plus slack
+    steps_total = a.warmup + 3 * a.steps + 8
     cfg = RunConfig(scheme="speculative", prompt_len=a.prompt, gen_len=steps_total, batch=a.batch,
                     speculation=SpeculationConfig(WORKLOAD["ratio"], WORKLOAD["alpha"], WORKLOAD["cap"], 1))
     eng = DecodeEngine(model, cfg, pool_dtype="f16", device=dev, group=group, fetch_ctas=a.fetch_ctas)
@@ -274,10 +277,29 @@ def run_b200(a) -> None:
         x_host.copy_(torch.from_numpy(out))
     barrier()
     e2e_ms = (time.perf_counter() - t0) * 1000.0
-    ms_t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=dev)
+    # -------- secondary variant: layer 0 (read in full every step) kept in HBM
+    var_ms = 0.0
+    var_stats = None
+    if not a.no_hbm_variant:
+        eng.set_hbm_layers(1)
+        for _ in range(2):
+            eng.decode_step()
+        eng.instrument(a.steps)
+        barrier()
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(cur)
+        for _ in range(a.steps):
+            eng.decode_step()
+        v1.record(cur)
+        barrier()
+        var_ms = v0.elapsed_time(v1)
+        var_stats = eng.kernel_stats()
+        eng._inst = None
+        eng.set_hbm_layers(0)
+    ms_t = torch.tensor([ms, e2e_ms, var_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms, e2e_ms = float(ms_t[0]), float(ms_t[1])
+    ms, e2e_ms, var_ms = float(ms_t[0]), float(ms_t[1]), float(ms_t[2])
 
     if rank == 0:
         tok = a.batch * a.steps
@@ -314,7 +336,17 @@ def run_b200(a) -> None:
                 "e2e": {"value": tok / (e2e_ms / 1000.0), "unit": UNIT,
                         "h2d_bytes_per_step": a.batch * spec.model_dim * 4,
                         "d2h_bytes_per_step": a.batch * spec.model_dim * 4},
-                "gpu_launches": launches, "setup_s": setup_s}
+                "gpu_launches": launches, "setup_s": setup_s,
+                "link_bytes_per_step": {"reference_accounted": _ref_bytes(stats, eng, a.steps),
+                                        "moved": f_bytes / a.steps}}
+        if var_stats is not None:
+            vk = [k for k in ("fetch_gather", "fetch_all_ce") if k in var_stats]
+            line["variant_layer0_in_hbm"] = {
+                "value": tok / (var_ms / 1000.0), "unit": UNIT, "ms_per_step": var_ms / a.steps,
+                "note": "same workload; layer 0's KV (1.3 GB, read in full every step) resident in HBM, "
+                        "layers 1-39 on the host pool",
+                "link_bytes_per_step_moved": sum(var_stats[k]["bytes"] for k in vk) / a.steps,
+                "kernel_stats": var_stats}
         if not a.no_cpu_baseline and world == 1:
             try:
                 line["cpu_baseline"] = cpu_reference(a.shape, a.batch, a.prompt, a.cpu_sample_steps)
@@ -324,6 +356,15 @@ def run_b200(a) -> None:
     eng.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def _ref_bytes(stats, eng, steps) -> float:
+    """The reference's LayerRecord.bytes summed over a step (engine.py:429):
+    layer 0 = all s rows, layers >= 1 = n rows, per head, 2*d*e bytes."""
+    n = stats["n_mean_per_layer"]
+    s = eng.s_host
+    per_row = eng.Hg * eng.row_bytes   # this rank's heads, pool element bytes
+    return float(eng.B * per_row * (s + sum(n[1:])))
 
 
 def _peak(key, fallback):

@@ -222,8 +222,7 @@ class DecodeEngine:
         D, F, kc = self.D, self.F, self.kcols
         i32, i64, f32 = torch.int32, torch.int64, torch.float32
         self.layer_bytes = B * Hg * S * self.row_bytes
-        host_layers = max(L - self.hbm_layers, 1)
-        self.pool = HostPool(host_layers * self.layer_bytes)
+        self.pool = HostPool(L * self.layer_bytes)
         T = _TORCH_ELT[self.elt]
         self.pool_hbm = (torch.zeros((self.hbm_layers, B, Hg, S, 2 * d), dtype=T, device=dev)
                          if self.hbm_layers else None)
@@ -252,9 +251,8 @@ class DecodeEngine:
         self.err = torch.zeros(1, dtype=i32, device=dev)
         self.pos = torch.zeros((L, B, Hg), dtype=i32, device=dev)
         self.events = torch.zeros((L, B, Hg, 2), dtype=i64, device=dev)
-        n_full = (0 if self.hbm_layers else 1) if spec_ else 2
         self.stage_full = [torch.empty((B, Hg, S, 2 * d), dtype=T, device=dev)
-                           for _ in range(n_full)]
+                           for _ in range(1 if spec_ else 2)]
         self.stage_sel = [torch.empty((B, Hg, cap, 2 * d), dtype=T, device=dev)
                           for _ in range(2 if spec_ else 0)]
         pf, tk = ctypes.c_size_t(), ctypes.c_size_t()
@@ -277,29 +275,52 @@ class DecodeEngine:
         self.s_host = s_len
 
     def pool_view(self) -> np.ndarray:
-        """Host pool as [L - hbm_layers][B][Hg][S_max][2][d] (no copy)."""
+        """Host pool as [L][B][Hg][S_max][2][d] (no copy).  Layers below
+        hbm_layers are authoritative in HBM (layer_rows reads either tier)."""
         npdt = {"f32": np.float32, "f16": np.float16, "bf16": np.uint16}[self.elt]
-        return self.pool.numpy(npdt, (max(self.L - self.hbm_layers, 1), self.B, self.Hg,
-                                      self.S_max, 2, self.d))
+        return self.pool.numpy(npdt, (self.L, self.B, self.Hg, self.S_max, 2, self.d))
 
     def layer_rows(self, li: int) -> np.ndarray:
         """Layer li's pool rows [B][Hg][S_max][2][d] as a host array (copy)."""
+        torch.cuda.synchronize(self.device)
         if li < self.hbm_layers:
             t = self.pool_hbm[li].view(self.B, self.Hg, self.S_max, 2, self.d)
             return (t.view(torch.uint16) if self.elt == "bf16" else t).cpu().numpy()
-        return np.array(self.pool_view()[li - self.hbm_layers])
+        return np.array(self.pool_view()[li])
+
+    def set_hbm_layers(self, n: int) -> None:
+        """Move layer 0's rows between the host pool and the HBM tier."""
+        if n not in (0, 1):
+            raise ValueError("hbm_layers must be 0 or 1")
+        torch.cuda.synchronize(self.device)
+        if n == self.hbm_layers:
+            return
+        T = _TORCH_ELT[self.elt]
+        if n == 1:
+            self.pool_hbm = torch.empty((1, self.B, self.Hg, self.S_max, 2 * self.d), dtype=T,
+                                        device=self.device)
+            _lib.call("ig_memcpy2d", self.pool_hbm.data_ptr(), self.layer_bytes, self.pool.host,
+                      self.layer_bytes, self.layer_bytes, 1, _lib.stream_handle(), kernels=0)
+        else:
+            _lib.call("ig_memcpy2d", self.pool.host, self.layer_bytes, self.pool_hbm.data_ptr(),
+                      self.layer_bytes, self.layer_bytes, 1, _lib.stream_handle(), kernels=0)
+        torch.cuda.synchronize(self.device)
+        if n == 0:
+            self.pool_hbm = None
+        self.hbm_layers = n
+        self._prefetched0 = False
 
     def _pool_layer_dev(self, li: int) -> int:
         """Device address of layer li's rows (HBM tier or the host pool alias)."""
         if li < self.hbm_layers:
             return self.pool_hbm[li].data_ptr()
-        return self.pool.dev + (li - self.hbm_layers) * self.layer_bytes
+        return self.pool.dev + li * self.layer_bytes
 
     def _pool_layer_host(self, li: int) -> int:
         """Copy-engine address of layer li's rows (UVA: host pointer or HBM)."""
         if li < self.hbm_layers:
             return self.pool_hbm[li].data_ptr()
-        return self.pool.host + (li - self.hbm_layers) * self.layer_bytes
+        return self.pool.host + li * self.layer_bytes
 
     # ---------------------------------------------------------- state import
     def load_state(self, x, kv, columns=None, meta=None) -> None:
@@ -332,11 +353,9 @@ class DecodeEngine:
                     elif self.elt == "bf16":
                         kb = torch.from_numpy(K).to(torch.bfloat16).view(torch.uint16).numpy()
                         vb = torch.from_numpy(V).to(torch.bfloat16).view(torch.uint16).numpy()
-                        lh = li - self.hbm_layers
-                        pv[lh, b, hl, :s, 0], pv[lh, b, hl, :s, 1] = kb, vb
+                        pv[li, b, hl, :s, 0], pv[li, b, hl, :s, 1] = kb, vb
                     else:
-                        lh = li - self.hbm_layers
-                        pv[lh, b, hl, :s, 0], pv[lh, b, hl, :s, 1] = K, V
+                        pv[li, b, hl, :s, 0], pv[li, b, hl, :s, 1] = K, V
                     if meta is not None and meta(li, b, h) is not None:
                         a_, l_, c_, sq = meta(li, b, h)
                         arr[li, b, hl, :s], lf[li, b, hl, :s], ct[li, b, hl, :s] = a_, l_, c_
@@ -520,6 +539,11 @@ class DecodeEngine:
         device (an engine buffer: valid until the next decode_step)."""
         if self.s_host < 1:
             raise RuntimeError("prefill has not run")
+        if self.config.pool_limit is None and self.s_host >= self.S_max:
+            # the reference grows its pool without bound; this one was sized at
+            # construction (prompt_len + max_steps rows) and must not overrun
+            raise ValueError(f"pool capacity {self.S_max} rows exhausted after "
+                             f"{self.iteration} steps: build the engine with a larger max_steps")
         cfg, spec = self.config, self.spec
         L, B, Hg, d = self.L, self.B, self.Hg, self.d
         Hgd = Hg * d

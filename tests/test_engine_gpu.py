@@ -288,9 +288,27 @@ def test_hbm_resident_layer0_is_identical(rname):
         try:
             outs.append(np.stack([eng.decode_step().cpu().numpy() for _ in range(ocfg.gen_len)]))
             recs.append(eng.records)
-            rows.append(eng.layer_rows(0))
+            rows.append(eng.layer_rows(0)[:, :, :eng.s_host])   # rows >= s are unused
         finally:
             eng.close()
     np.testing.assert_array_equal(outs[0], outs[1])
     assert recs[0] == recs[1]
     np.testing.assert_array_equal(rows[0], rows[1])   # appends / evictions land alike
+
+
+def test_pool_capacity_is_enforced():
+    """Decoding past prompt_len + max_steps rows raises instead of overrunning."""
+    from paper_2406_19707_b200 import DecodeEngine
+    _, sk = models("m64")
+    ocfg = run_config("spec", batch=1, gen_len=2)
+    sessions = oracle_sessions(sk, ocfg)
+    eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg), sessions, pool_dtype="f32", max_steps=2)
+    try:
+        steps = 0
+        with pytest.raises(ValueError, match="capacity"):
+            for _ in range(10):
+                eng.decode_step()
+                steps += 1
+        assert steps == eng.S_max - ocfg.prompt_len     # every row up to S_max is usable
+    finally:
+        eng.close()
