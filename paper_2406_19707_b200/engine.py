@@ -516,6 +516,63 @@ class DecodeEngine:
         out["n_mean_per_layer"] = [float(x) for x in n_hist[:inst["k"]].mean(axis=(0, 2))]
         return out
 
+    @torch.no_grad()
+    def isolated_kernel_times(self, li: int = 1, reps: int = 5) -> dict:
+        """Time the compute-stream path kernels of layer li one at a time with
+        nothing else on the GPU (CUDA events, best of `reps`), on the engine's
+        current state: the HBM-bound kernels' own roofline, free of the
+        concurrent gather.  Leaves the decode state unchanged (scores,
+        count_sum and the attention output are scratch)."""
+        if self.scheme != "speculative" or not (1 <= li < self.L):
+            raise ValueError("needs a speculative layer >= 1")
+        torch.cuda.synchronize(self.device)
+        B, Hg, d, S, kc = self.B, self.Hg, self.d, self.S_max, self.kcols
+        s = self.s_host
+        sc = self.config.speculation
+        cs = torch.cuda.current_stream(self.device)
+        h = cs.cuda_stream
+        Hgd = Hg * d
+        n_tot = int(self.n[li].sum().item())
+
+        def best(fn):
+            t = []
+            for _ in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(cs)
+                fn()
+                e1.record(cs)
+                e1.synchronize()
+                t.append(e0.elapsed_time(e1))
+            return min(t)
+
+        def rehearse():
+            self.count_sum[li].zero_()
+            _lib.call("ig_rehearse_count", self.qspec.data_ptr(), Hgd, self.cols[li].data_ptr(),
+                      self.pk[li - 1].data_ptr(), self.st.data_ptr(), B, Hg, d, kc, S, self.scale,
+                      float(sc.alpha), 0, self.scores.data_ptr(), self.counts.data_ptr(),
+                      self.count_sum[li].data_ptr(), h)
+
+        idx_tmp = torch.empty_like(self.idx[li])
+        n_tmp = torch.empty_like(self.n[li])
+
+        def select():
+            _lib.call("ig_select", self.scores.data_ptr(), self.count_sum[li].data_ptr(),
+                      self.st.data_ptr(), B, Hg, self.H, S, self.cap, float(sc.cap_ratio),
+                      int(sc.min_select), idx_tmp.data_ptr(), n_tmp.data_ptr(), self.err.data_ptr(), h)
+
+        def attend():
+            self._attend(li, self.stage_sel[li % 2], self.idx[li], self.n[li], self.cap, h)
+
+        rows = [("rehearse_count", rehearse, 4 * B * Hg * s * (kc + 1)),
+                ("select", select, 4 * B * Hg * s),
+                ("attend", attend, n_tot * Hg * self.row_bytes)]
+        out = {}
+        for name, fn, nbytes in rows:
+            ms = best(fn)
+            out[name] = {"ms": ms, "bytes": nbytes, "gbs": nbytes / (ms * 1e6)}
+        torch.cuda.synchronize(self.device)
+        return out
+
     # ----------------------------------------------------------------- decode
     def _issue_full_fetch(self, li: int, s: int, stage: torch.Tensor) -> None:
         self._mark("fetch", li, self.fetch_stream, True)

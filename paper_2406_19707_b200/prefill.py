@@ -31,9 +31,21 @@ def layernorm(x: torch.Tensor, gain: torch.Tensor, bias: torch.Tensor, eps: floa
     return y
 
 
-def causal_attention(q, k, v):
-    """softmax(q k^T / sqrt(d)) v with a causal mask; q, k, v: [H, N, d] f32."""
-    return F.scaled_dot_product_attention(q, k, v, is_causal=True)
+def causal_attention(q, k, v, block: int = 2048):
+    """softmax(q k^T / sqrt(d)) v with a causal mask; q, k, v: [H, N, d] f32.
+
+    Long prompts go in query blocks: f32 SDPA may fall back to the math path,
+    which would materialise H x N x N scores (128 GiB at 32 heads x 32K)."""
+    n = q.shape[-2]
+    if n <= block:
+        return F.scaled_dot_product_attention(q, k, v, is_causal=True)
+    out = torch.empty_like(q)
+    for r0 in range(0, n, block):
+        r1 = min(n, r0 + block)
+        mask = torch.ones(r1 - r0, r1, dtype=torch.bool, device=q.device).tril(r0)
+        out[..., r0:r1, :] = F.scaled_dot_product_attention(q[..., r0:r1, :], k[..., :r1, :],
+                                                             v[..., :r1, :], attn_mask=mask)
+    return out
 
 
 def dense_block_forward(x: torch.Tensor, lw, spec):

@@ -206,3 +206,16 @@ def test_rehearse_count_fused_matches_oracle(cluster, s):
             v = got_s[b, h]
             assert got_c[b, h] == int(np.sum(v > (float(np.max(v)) - alpha)))
         assert int(csum[b]) == int(got_c[b].sum())
+
+
+def test_blocked_causal_prefill_attention_matches_oracle():
+    """The query-blocked causal attention used for long prompts == model.py:156-180."""
+    import torch
+    from paper_2406_19707_b200.prefill import causal_attention
+    rng = np.random.default_rng(4)
+    H, N, d = 3, 300, 16
+    q, k, v = (rng.standard_normal((H, N, d)).astype(np.float32) for _ in range(3))
+    got = causal_attention(*(torch.from_numpy(a).cuda() for a in (q, k, v)), block=64).cpu().numpy()
+    for h in range(H):
+        ref, _ = O.attention_head(q[h], k[h], v[h], causal=True)
+        np.testing.assert_allclose(got[h], ref, rtol=1e-4, atol=1e-5)
