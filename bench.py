@@ -54,6 +54,10 @@ def _args():
     ap.add_argument("--shape", default=WORKLOAD["shape"])
     ap.add_argument("--layers", type=int, default=None, help="override (debug only)")
     ap.add_argument("--fetch-ctas", type=int, default=32)
+    ap.add_argument("--fetch-threads", type=int, default=32)
+    ap.add_argument("--fetch-priority", type=int, default=0, help="CUDA stream priority (-1 = high)")
+    ap.add_argument("--fetch-impl", default="tma", choices=["ldg", "tma"])
+    ap.add_argument("--fetch-rows", type=int, default=16, help="TMA rows per warp batch")
     ap.add_argument("--no-hbm-variant", action="store_true",
                     help="skip the secondary run with layer 0's KV resident in HBM")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -192,6 +196,8 @@ def _config(a) -> dict:
             "global_batch": a.batch, "context": a.prompt, "partial_ratio": WORKLOAD["ratio"],
             "alpha": WORKLOAD["alpha"], "cap_ratio": WORKLOAD["cap"],
             "outlier_scale": WORKLOAD["outlier_scale"], "kv_pool": "pinned host, f16",
+            "fetch": (f"{a.fetch_impl} x {a.fetch_ctas} CTAs x {a.fetch_threads} threads"
+                      + (f" x {a.fetch_rows} rows/batch" if a.fetch_impl == "tma" else "")),
             "parallelism": f"tp{a.gpus} (heads)" if a.gpus > 1 else "single GPU",
             "l2": "inputs larger than L2 (partial K >= 1.6 GB streamed per layer set; host pool 54 GB)"}
 
@@ -226,7 +232,9 @@ def run_b200(a) -> None:
     steps_total = a.warmup + 3 * a.steps + 8
     cfg = RunConfig(scheme="speculative", prompt_len=a.prompt, gen_len=steps_total, batch=a.batch,
                     speculation=SpeculationConfig(WORKLOAD["ratio"], WORKLOAD["alpha"], WORKLOAD["cap"], 1))
-    eng = DecodeEngine(model, cfg, pool_dtype="f16", device=dev, group=group, fetch_ctas=a.fetch_ctas)
+    eng = DecodeEngine(model, cfg, pool_dtype="f16", device=dev, group=group, fetch_ctas=a.fetch_ctas,
+                       fetch_threads=a.fetch_threads, fetch_priority=a.fetch_priority,
+                       fetch_impl=a.fetch_impl, fetch_rows=a.fetch_rows)
     # engine holds its own (sharded) copies: drop the full model
     del model
     torch.cuda.empty_cache()
@@ -312,7 +320,8 @@ def run_b200(a) -> None:
         f_ms = sum(stats[k]["ms"] for k in fetch_keys)
         f_launch = sum(stats[k]["launches"] for k in fetch_keys)
         fetch_gbs = f_bytes / (f_ms * 1e6) if f_ms else None
-        roof = {"kernel": "fetch (ig_fetch zero-copy gather + ig_fetch_all copy-engine rows)",
+        roof = {"kernel": f"fetch (ig_fetch{'_tma' if a.fetch_impl == 'tma' else ''} gather + "
+                          "ig_fetch_all copy-engine rows)",
                 "bound": "host_link", "achieved": fetch_gbs, "peak": link_peak["gbs"],
                 "peak_source": link_peak["source"], "unit": "GB/s",
                 "frac": (fetch_gbs / link_peak["gbs"]) if fetch_gbs else None, "traffic": None,

@@ -121,7 +121,16 @@ int ig_topk_rows(const float* values, int rows, int len, int k, int32_t* idx_out
  * Zero-copy SM gather of the selected rows from the mapped host pool into
  * stage.  pool_dev = device alias of this layer's T[B][Hg][S_max][2][d].   */
 int ig_fetch(const void* pool_dev, const int32_t* idx, const int32_t* n, int B, int Hg,
-             int S_max, int cap, int row_bytes, void* stage, int ctas, void* stream);
+             int S_max, int cap, int row_bytes, void* stage, int ctas, int threads,
+             void* stream);   /* threads per CTA: 256, 512 or 1024 */
+/* Same gather with TMA bulk copies (host -> smem -> HBM): `warps` (1-4) warps
+ * per CTA; each warp moves `rows_per_batch` (<= 32) rows per batch, one per
+ * lane, with two batches loading while the previous one drains (shared memory
+ * warps * 3 * rows_per_batch * row_bytes).  The bytes in flight live in shared
+ * memory, so the gather takes almost no threads/registers from compute.     */
+int ig_fetch_tma(const void* pool_dev, const int32_t* idx, const int32_t* n, int B, int Hg,
+                 int S_max, int cap, int row_bytes, void* stage, int ctas, int warps,
+                 int rows_per_batch, void* stream);
 /* Layer 0 (engine.py:393-396): every row [0, s) by copy engine, host sizes. */
 int ig_fetch_all(const void* pool_host, int B, int Hg, int S_max, int s, int row_bytes,
                  void* stage, int stage_rows, void* stream);

@@ -237,7 +237,7 @@ extern "C" int ig_rehearse_count(const float* qspec, int ldq, const int32_t* col
   const int quads = S_max / 4;
   const size_t smem = (size_t)((quads + C - 1) / C) * sizeof(float4);
   if (smem > 200 * 1024) return IG_EINVAL;
-  if (smem > 48 * 1024)
+  if (smem > 32 * 1024)  // dynamic + static must fit: opt in early
     IG_CUDA_STATUS(cudaFuncSetAttribute(rehearse_count_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};

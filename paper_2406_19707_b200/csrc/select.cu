@@ -206,7 +206,7 @@ extern "C" int ig_select(const float* scores, const int32_t* count_sum, const ig
     return IG_EINVAL;
   const size_t smem = (size_t)S_max * 4;  // the row's order keys
   if (smem > kSelMaxSmem) return IG_EINVAL;
-  if (smem > 48 * 1024)
+  if (smem > 32 * 1024)  // dynamic + static must fit: opt in early
     IG_CUDA_STATUS(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
   select_kernel<<<dim3(Hg, B), kSelThreads, smem, (cudaStream_t)stream>>>(
@@ -222,7 +222,7 @@ extern "C" int ig_order_by_score(const float* scores, const int32_t* n, int B, i
   if (B < 1 || Hg < 1 || cap < 1 || !scores || !n || !idx) return IG_EINVAL;
   const size_t smem = (size_t)cap * 8;
   if (smem > 200 * 1024) return IG_EINVAL;
-  if (smem > 48 * 1024)
+  if (smem > 32 * 1024)  // dynamic + static must fit: opt in early
     IG_CUDA_STATUS(cudaFuncSetAttribute(order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
   order_kernel<<<dim3(Hg, B), 256, smem, (cudaStream_t)stream>>>(scores, n, Hg, S_max, cap, idx);
@@ -237,7 +237,7 @@ extern "C" int ig_topk_rows(const float* values, int rows, int len, int k, int32
   if (k == 0) return IG_OK;
   const size_t smem = (size_t)len * 4;
   if (smem > kSelMaxSmem) return IG_EINVAL;
-  if (smem > 48 * 1024)
+  if (smem > 32 * 1024)  // dynamic + static must fit: opt in early
     IG_CUDA_STATUS(cudaFuncSetAttribute(topk_rows_kernel,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   topk_rows_kernel<<<rows, kSelThreads, smem, (cudaStream_t)stream>>>(values, len, k, idx_out);

@@ -147,7 +147,14 @@ class DecodeEngine:
     max_steps : decode steps to size the pool for (default config.gen_len)
     pool_dtype : "f16" (default, e = 2 bytes), "bf16" or "f32"
     group : torch.distributed process group for head tensor parallelism
-    fetch_ctas : CTAs of the zero-copy gather (the rest of the GPU computes)
+    fetch_ctas, fetch_threads : gather grid (the rest of the GPU computes)
+    fetch_priority : CUDA priority of the fetch stream (lower = more urgent),
+        so gather CTAs win free SM slots over compute-stream CTAs
+    fetch_impl : "tma" (default: bulk async copies through shared memory,
+        fetch_threads/32 warps per CTA, fetch_rows rows per warp batch) or
+        "ldg" (16-B vector loads through registers, fetch_threads per CTA).
+        Defaults (32 CTAs x 1 warp x 16 rows) come from tools/sweep_fetch.sh on
+        C2 and C3 (profiles/r01_fetch_sweep.md).
     hbm_layers : 0 (default: every layer's KV in the pinned host pool) or 1:
         keep layer 0's rows -- which every step reads in full (engine.py:393-396)
         -- resident in HBM, so they never cross the host link.  Traces keep the
@@ -156,7 +163,8 @@ class DecodeEngine:
 
     def __init__(self, model, config: RunConfig, *, max_steps: int | None = None,
                  pool_dtype: str = "f16", device=None, group=None, fetch_ctas: int = 32,
-                 hbm_layers: int = 0):
+                 fetch_threads: int = 32, fetch_priority: int = 0, hbm_layers: int = 0,
+                 fetch_impl: str = "tma", fetch_rows: int = 16):
         config.validate()
         _lib.load()
         _enable_ieee_fp32()
@@ -190,6 +198,12 @@ class DecodeEngine:
         self.cap = max(int(math.floor(sc.cap_ratio * self.S_max)), sc.min_select, 1)
         self.policy = EvictionPolicy(config.pool_policy)
         self.fetch_ctas = fetch_ctas
+        self.fetch_threads = fetch_threads
+        self.fetch_priority = fetch_priority
+        if fetch_impl not in ("ldg", "tma"):
+            raise ValueError("fetch_impl must be 'ldg' or 'tma'")
+        self.fetch_impl = fetch_impl
+        self.fetch_rows = fetch_rows
         if hbm_layers not in (0, 1) or hbm_layers > spec.layers:
             raise ValueError("hbm_layers must be 0 or 1")
         self.hbm_layers = hbm_layers
@@ -260,7 +274,7 @@ class DecodeEngine:
         self.att_partial = torch.empty(pf.value, dtype=f32, device=dev)
         self.att_tickets = torch.zeros(tk.value, dtype=i32, device=dev)
         self.compute = torch.cuda.Stream(device=dev)
-        self.fetch_stream = torch.cuda.Stream(device=dev)
+        self.fetch_stream = torch.cuda.Stream(device=dev, priority=self.fetch_priority)
         self.ev_sel = [torch.cuda.Event() for _ in range(L)]
         self.ev_fetch = [torch.cuda.Event() for _ in range(L)]
         self.ev_att = [torch.cuda.Event() for _ in range(L)]
@@ -652,10 +666,18 @@ class DecodeEngine:
                         self.ev_sel[nxt].record(C)
                         Fs.wait_event(self.ev_sel[nxt])
                         self._mark("fetch", nxt, Fs, True)
-                        _lib.call("ig_fetch", self._pool_layer_dev(nxt), self.idx[nxt].data_ptr(),
-                                  self.n[nxt].data_ptr(), B, Hg, self.S_max, self.cap,
-                                  self.row_bytes, self.stage_sel[nxt % 2].data_ptr(),
-                                  self.fetch_ctas, Fs.cuda_stream)
+                        if self.fetch_impl == "tma":
+                            _lib.call("ig_fetch_tma", self._pool_layer_dev(nxt),
+                                      self.idx[nxt].data_ptr(), self.n[nxt].data_ptr(), B, Hg,
+                                      self.S_max, self.cap, self.row_bytes,
+                                      self.stage_sel[nxt % 2].data_ptr(), self.fetch_ctas,
+                                      max(1, self.fetch_threads // 32), self.fetch_rows,
+                                      Fs.cuda_stream)
+                        else:
+                            _lib.call("ig_fetch", self._pool_layer_dev(nxt), self.idx[nxt].data_ptr(),
+                                      self.n[nxt].data_ptr(), B, Hg, self.S_max, self.cap,
+                                      self.row_bytes, self.stage_sel[nxt % 2].data_ptr(),
+                                      self.fetch_ctas, self.fetch_threads, Fs.cuda_stream)
                         self._mark("fetch", nxt, Fs, False)
                     else:
                         if li >= 1:

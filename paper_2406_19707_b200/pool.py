@@ -141,7 +141,7 @@ class KvPool:
             di = torch.from_numpy(idx.astype(np.int32)).to(self._dev)
             nn = torch.tensor([idx.size], dtype=torch.int32, device=self._dev)
             _lib.call("ig_fetch", self._host.dev, di.data_ptr(), nn.data_ptr(), 1, 1,
-                      self.capacity, idx.size, self.row_bytes, out.data_ptr(), 1, hs)
+                      self.capacity, idx.size, self.row_bytes, out.data_ptr(), 1, 256, hs)
             uniq = np.unique(idx).astype(np.int32)   # numpy fancy-index assignment: once per row
             du = torch.from_numpy(uniq).to(self._dev)
             nu = torch.tensor([uniq.size], dtype=torch.int32, device=self._dev)

@@ -49,7 +49,7 @@ def test_argument_validation_without_gpu(lib):
     P = None
     assert lib.ig_rehearse(P, 0, P, P, P, 0, 1, 1, 1, 4, 1.0, P, P, P) == _lib.IG_EINVAL
     assert lib.ig_select(P, P, P, 1, 1, 1, 4, 1, 0.2, 1, P, P, P, P) == _lib.IG_EINVAL
-    assert lib.ig_fetch(P, P, P, 1, 1, 4, 1, 512, P, 1, P) == _lib.IG_EINVAL
+    assert lib.ig_fetch(P, P, P, 1, 1, 4, 1, 512, P, 1, 256, P) == _lib.IG_EINVAL
     assert lib.ig_attend(P, 0, P, P, 0, P, 0, P, P, P, P, 1, 1, 128, 4, P, P, P, 0, P) == _lib.IG_EINVAL
     assert lib.ig_count(P, P, P, 1, 1, 4, -1.0, P, P, P) == _lib.IG_EINVAL
     sz, tk = ctypes.c_size_t(), ctypes.c_size_t()

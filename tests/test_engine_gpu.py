@@ -312,3 +312,22 @@ def test_pool_capacity_is_enforced():
         assert steps == eng.S_max - ocfg.prompt_len     # every row up to S_max is usable
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("impl,ctas,threads,rows", [("tma", 8, 32, 32), ("tma", 3, 128, 5),
+                                                    ("ldg", 5, 256, 32)])
+def test_fetch_implementations_identical(impl, ctas, threads, rows):
+    """Every gather implementation/geometry yields the same decode, bit for bit."""
+    from paper_2406_19707_b200 import DecodeEngine
+    _, sk = models("m256")
+    ocfg = run_config("spec", record_selection=True)
+    sessions = oracle_sessions(sk, ocfg)
+    outs = []
+    for kw in ({}, dict(fetch_impl=impl, fetch_ctas=ctas, fetch_threads=threads, fetch_rows=rows)):
+        eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg), copy.deepcopy(sessions),
+                                         pool_dtype="f16", **kw)
+        try:
+            outs.append(np.stack([eng.decode_step().cpu().numpy() for _ in range(ocfg.gen_len)]))
+        finally:
+            eng.close()
+    np.testing.assert_array_equal(outs[0], outs[1])
