@@ -75,14 +75,14 @@ int ig_rehearse(const float* qspec, int ldq, const int32_t* cols, const float* p
                 float scale, float* scores, uint32_t* maxkey, void* stream);
 
 /* ---- K1+K2a fused (engine path): ig_rehearse + ig_count in one launch ----
- * One thread-block cluster of `cluster` CTAs per (b, h) row (0 = auto, <= 8):
- * the row's partial-K columns are streamed once, the per-CTA maxima and then
- * the alpha counts are exchanged through distributed shared memory.  Writes
- * scores (for ig_select), counts[b,h] and count_sum[b] += (zero it first).   */
+ * The rehearsal tiles max-reduce into maxkey[b,h] and take a ticket; the last
+ * tile of each (b, h) row counts score > float32(double(max) - alpha) over the
+ * row and adds it to count_sum[b] (zero that first).  maxkey and tickets are
+ * [B][Hg] scratch that must start zeroed and are left zeroed.               */
 int ig_rehearse_count(const float* qspec, int ldq, const int32_t* cols, const float* pk,
                       const ig_step_state* st, int B, int Hg, int d, int k, int S_max,
-                      float scale, double alpha, int cluster, float* scores, int32_t* counts,
-                      int32_t* count_sum, void* stream);
+                      float scale, double alpha, float* scores, uint32_t* maxkey,
+                      int32_t* tickets, int32_t* counts, int32_t* count_sum, void* stream);
 
 /* Row maxima (as order keys) of scores not produced by ig_rehearse (the
  * select_tokens shim, speculation.py:156).                                  */

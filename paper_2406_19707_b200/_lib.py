@@ -32,7 +32,7 @@ _SIGS = {
     "ig_host_alloc": [_SZ, ctypes.POINTER(_P), ctypes.POINTER(_P)],
     "ig_host_free": [_P],
     "ig_rehearse": [_P, _I, _P, _P, _P, _I, _I, _I, _I, _I, _F, _P, _P, _P],
-    "ig_rehearse_count": [_P, _I, _P, _P, _P, _I, _I, _I, _I, _I, _F, _D, _I, _P, _P, _P, _P],
+    "ig_rehearse_count": [_P, _I, _P, _P, _P, _I, _I, _I, _I, _I, _F, _D, _P, _P, _P, _P, _P, _P],
     "ig_count": [_P, _P, _P, _I, _I, _I, _D, _P, _P, _P],
     "ig_select": [_P, _P, _P, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P],
     "ig_order_by_score": [_P, _P, _I, _I, _I, _I, _P, _P],

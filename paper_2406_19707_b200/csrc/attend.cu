@@ -231,33 +231,74 @@ attend512_kernel(const float* __restrict__ q, int ldq, const float* __restrict__
 
   const int r0 = c * kFastChunk, r1 = min(rows, r0 + kFastChunk);
   const uint4* base = reinterpret_cast<const uint4*>(stage + bh * (size_t)cap * 2 * d);
-  for (int rb = r0 + w * kFastRows; rb < r1; rb += kAttWarps * kFastRows) {
-    uint4 raw[kFastRows];
-    int rowid = 0;
+  // Rows go in groups of kFastRows per warp.  The next group's loads are in
+  // flight while the current group is folded into the softmax, and a group is
+  // folded at once: kFastRows independent dot products / shuffle reductions,
+  // one running-max update, one rescale of (l, acc).
+  auto load_group = [&](int rb, uint4* raw, int& rowid) {
+    rowid = 0;
     if (idx && lane < kFastRows && rb + lane < r1) rowid = idx[bh * cap + rb + lane];
 #pragma unroll
     for (int u = 0; u < kFastRows; ++u) {
-      const int r = rb + u;
-      if (r < r1) {
+      if (rb + u < r1)
         asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(raw[u].x), "=r"(raw[u].y), "=r"(raw[u].z), "=r"(raw[u].w)
-                     : "l"(base + (size_t)r * 32 + lane));
-      }
+                     : "l"(base + (size_t)(rb + u) * 32 + lane));
+      else  // a p = 0 weight times stale register bits could be 0 * NaN
+        raw[u] = make_uint4(0u, 0u, 0u, 0u);
     }
+  };
+  const int step = kAttWarps * kFastRows;
+  int rb = r0 + w * kFastRows;
+  uint4 raw[kFastRows], nxt[kFastRows];
+  int rowid = 0, nrowid = 0;
+  if (rb < r1) load_group(rb, raw, rowid);
+  for (; rb < r1; rb += step) {
+    if (rb + step < r1) load_group(rb + step, nxt, nrowid);
+    float dot[kFastRows];
 #pragma unroll
     for (int u = 0; u < kFastRows; ++u) {
-      const int r = rb + u;
-      const int id = idx ? __shfl_sync(0xffffffffu, rowid, u) : r;
-      if (r >= r1 || id == pos) continue;   // warp-uniform
       float f[8];
       unpack8<T>(raw[u], f);
-      float dot = 0.f;
-      if (klane) {
+      float a = 0.f;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) dot = fmaf(qv[i], f[i], dot);
-      }
-      consume(dot, f);
+      for (int i = 0; i < 8; ++i) a = fmaf(qv[i], f[i], a);
+      dot[u] = klane ? a : 0.f;
     }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+#pragma unroll
+      for (int u = 0; u < kFastRows; ++u) dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], o);
+    }
+    float gm = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < kFastRows; ++u) {
+      const int id = idx ? __shfl_sync(0xffffffffu, rowid, u) : rb + u;
+      const bool ok = rb + u < r1 && id != pos;
+      dot[u] = ok ? __shfl_sync(0xffffffffu, dot[u], 0) / sqrt_d : -INFINITY;
+      gm = fmaxf(gm, dot[u]);
+    }
+    if (gm != -INFINITY) {        // warp-uniform
+      const float mn = fmaxf(m, gm);
+      const float corr = expf(m - mn);
+      float psum = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] *= corr;
+#pragma unroll
+      for (int u = 0; u < kFastRows; ++u) {
+        const float p = expf(dot[u] - mn);   // exp(-inf) = 0 for skipped rows
+        psum += p;
+        float f[8];
+        unpack8<T>(raw[u], f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fmaf(p, f[i], acc[i]);
+      }
+      l = l * corr + psum;
+      m = mn;
+    }
+#pragma unroll
+    for (int u = 0; u < kFastRows; ++u) raw[u] = nxt[u];
+    rowid = nrowid;
   }
   if (c == 0 && w == 0) {  // the current token: GPU-resident f32 row
     const float* src = (klane ? k_cur : v_cur) + (size_t)b * ldkv + (size_t)h * d + e0;

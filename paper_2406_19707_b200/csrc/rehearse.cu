@@ -6,11 +6,7 @@
 // its cols-subset) and pk is the partial key cache stored column-major over
 // tokens, so a warp's 32 x float4 loads of one column j are one 512-B burst.
 // HBM-bound: each launch streams 4*k*s bytes per (b, h) once.
-#include <cooperative_groups.h>
-
 #include "common.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace ig {
 
@@ -123,49 +119,44 @@ score_max_kernel(const float* __restrict__ scores, const ig_step_state* __restri
   }
 }
 
-// Fused rehearsal + alpha count (speculation.py:133-134 and :154-157) for one
-// (b, h) score row split across a thread-block cluster of C CTAs: each CTA
-// scores its contiguous token range (kept in shared memory and written out for
-// ig_select), the CTAs exchange their maxima through distributed shared memory,
-// then count score > float32(double(max) - alpha) locally and rank 0 sums the
-// C counts.  Replaces ig_rehearse + ig_count (+ the maxkey memset) on the
-// engine path; the row is read from HBM exactly once.
-constexpr int kFusedThreads = 256;
-
-__global__ void __launch_bounds__(kFusedThreads)
+// Fused rehearsal + alpha count (speculation.py:133-134 and :154-157).  The
+// rehearsal CTAs are the plain 1024-token tiles of rehearse_kernel (no
+// clusters: ~2.7 waves at C3, the shape that streams partial K at ~0.9 of
+// HBM peak); each max-reduces its tile into maxkey[b,h] and takes a ticket, and
+// the LAST tile of a row to finish counts score > float32(double(max) - alpha)
+// over the row (L2-resident, just written), adds it to count_sum[b] and resets
+// the row's maxkey/ticket for the next launch.  A cluster/DSMEM version of
+// the same fusion measured slower (wave quantization of 2-CTA clusters).
+__global__ void __launch_bounds__(kRehearseThreads)
 rehearse_count_kernel(const float* __restrict__ qspec, int ldq, const int32_t* __restrict__ cols,
                       const float* __restrict__ pk, const ig_step_state* __restrict__ st, int Hg,
                       int d, int k, int S_max, float scale, double alpha,
-                      float* __restrict__ scores, int32_t* __restrict__ counts,
+                      float* __restrict__ scores, uint32_t* __restrict__ maxkey,
+                      int32_t* __restrict__ tickets, int32_t* __restrict__ counts,
                       int32_t* __restrict__ count_sum) {
-  cg::cluster_group cluster = cg::this_cluster();
-  const int C = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
-  extern __shared__ float4 sc_local[];
-  __shared__ float qs[kMaxK];
-  __shared__ uint32_t red_u[kFusedThreads / kWarp];
-  __shared__ int red_i[kFusedThreads / kWarp];
-  __shared__ uint32_t cta_max;
-  __shared__ int cta_count;
   const int b = blockIdx.z, h = blockIdx.y;
-  const size_t bh = (size_t)b * Hg + h;
   const int s = st->s_len;
-  const int quads = (s + 3) >> 2;
-  const int per = (quads + C - 1) / C;
-  const int q0 = rank * per, q1 = min(quads, q0 + per);
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int j = tid; j < k; j += blockDim.x)
+  const int t0 = blockIdx.x * kRehearseChunk;
+  const int tiles = (s + kRehearseChunk - 1) / kRehearseChunk;
+  if (t0 >= s) return;
+  __shared__ float qs[kMaxK];
+  __shared__ uint32_t wmax[kRehearseThreads / kWarp];
+  __shared__ int red[kRehearseThreads / kWarp];
+  __shared__ int last;
+  const size_t bh = (size_t)b * Hg + h;
+  for (int j = threadIdx.x; j < k; j += blockDim.x)
     qs[j] = qspec[(size_t)b * ldq + (size_t)h * d + cols[bh * k + j]];
   __syncthreads();
 
-  const float* base = pk + bh * (size_t)k * S_max;
-  float* out = scores + bh * S_max;
+  const int t = t0 + threadIdx.x * kRehearseTok;
+  const float* base = pk + bh * (size_t)k * S_max + t;
+  float* row = scores + bh * S_max;
   uint32_t kmax = 0;
-  for (int qd = q0 + tid; qd < q1; qd += blockDim.x) {
-    const int t = qd * 4;
+  if (t < s) {
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll 8
     for (int j = 0; j < k; ++j) {
-      const float4 v = ldg_stream(reinterpret_cast<const float4*>(base + (size_t)j * S_max + t));
+      const float4 v = ldg_stream(reinterpret_cast<const float4*>(base + (size_t)j * S_max));
       const float q = qs[j];
       a0 = fmaf(q, v.x, a0);
       a1 = fmaf(q, v.y, a1);
@@ -173,87 +164,57 @@ rehearse_count_kernel(const float* __restrict__ qspec, int ldq, const int32_t* _
       a3 = fmaf(q, v.w, a3);
     }
     float4 r = make_float4(a0 * scale, a1 * scale, a2 * scale, a3 * scale);
-    // tokens >= s (tail of the last quad) never count and never win the max
-    if (t + 1 >= s) r.y = -INFINITY;
+    if (t + 1 >= s) r.y = -INFINITY;  // tail of the last quad: never counts, never the max
     if (t + 2 >= s) r.z = -INFINITY;
     if (t + 3 >= s) r.w = -INFINITY;
-    sc_local[qd - q0] = r;
-    *reinterpret_cast<float4*>(out + t) = r;  // S_max % 4 == 0: in bounds
-    kmax = max(kmax, max(max(order_key(r.x), order_key(r.y)), max(order_key(r.z), order_key(r.w))));
+    *reinterpret_cast<float4*>(row + t) = r;   // S_max % 4 == 0: in bounds
+    kmax = max(max(order_key(r.x), order_key(r.y)), max(order_key(r.z), order_key(r.w)));
   }
   kmax = warp_max_u32(kmax);
-  if (lane == 0) red_u[w] = kmax;
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = kmax;
   __syncthreads();
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     uint32_t m = 0;
-    for (int i = 0; i < kFusedThreads / kWarp; ++i) m = max(m, red_u[i]);
-    cta_max = m;
+    for (int i = 0; i < kRehearseThreads / kWarp; ++i) m = max(m, wmax[i]);
+    atomicMax(maxkey + bh, m);       // max is order-independent: exact
+    __threadfence();                 // my scores and max before my ticket
+    last = atomicAdd(tickets + bh, 1) == tiles - 1;
   }
-  cluster.sync();
-  uint32_t gkey = 0;
-  for (int r = 0; r < C; ++r) gkey = max(gkey, *cluster.map_shared_rank(&cta_max, r));
-  const float thr = __double2float_rn((double)key_to_float(gkey) - alpha);
-  int c = 0;
-  for (int qd = q0 + tid; qd < q1; qd += blockDim.x) {
-    const float4 r = sc_local[qd - q0];
-    c += (r.x > thr) + (r.y > thr) + (r.z > thr) + (r.w > thr);
-  }
-  c = warp_sum(c);
-  if (lane == 0) red_i[w] = c;
   __syncthreads();
-  if (tid == 0) {
-    int t = 0;
-    for (int i = 0; i < kFusedThreads / kWarp; ++i) t += red_i[i];
-    cta_count = t;
+  if (!last) return;
+  __threadfence();
+  const float thr = __double2float_rn((double)key_to_float(__ldcg(maxkey + bh)) - alpha);
+  int c = 0;
+  for (int i = threadIdx.x * 4; i < s; i += blockDim.x * 4) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(row + i));
+    c += (v.x > thr) + (v.y > thr) + (v.z > thr) + (v.w > thr);
   }
-  cluster.sync();
-  if (rank == 0 && tid == 0) {
-    int t = 0;
-    for (int r = 0; r < C; ++r) t += *cluster.map_shared_rank(&cta_count, r);
-    counts[bh] = t;
-    atomicAdd(count_sum + b, t);
+  c = block_sum(c, red);
+  if (threadIdx.x == 0) {
+    counts[bh] = c;
+    atomicAdd(count_sum + b, c);     // integer: exact, order-free
+    maxkey[bh] = 0;                  // scratch ready for the next launch
+    tickets[bh] = 0;
   }
-  cluster.sync();  // peers' shared memory stays alive until rank 0 has read it
 }
 
 }  // namespace ig
 
 extern "C" int ig_rehearse_count(const float* qspec, int ldq, const int32_t* cols, const float* pk,
                                  const ig_step_state* st, int B, int Hg, int d, int k, int S_max,
-                                 float scale, double alpha, int cluster, float* scores,
-                                 int32_t* counts, int32_t* count_sum, void* stream) {
+                                 float scale, double alpha, float* scores, uint32_t* maxkey,
+                                 int32_t* tickets, int32_t* counts, int32_t* count_sum,
+                                 void* stream) {
   using namespace ig;
   if (B < 1 || Hg < 1 || d < 1 || k < 1 || k > d || k > kMaxK || S_max < 1 || (S_max & 3) ||
-      ldq < Hg * d || !(alpha > 0) || !qspec || !cols || !pk || !st || !scores || !counts ||
-      !count_sum)
+      ldq < Hg * d || !(alpha > 0) || !qspec || !cols || !pk || !st || !scores || !maxkey ||
+      !tickets || !counts || !count_sum)
     return IG_EINVAL;
-  int C = cluster;
-  if (C <= 0) {  // enough CTAs for ~8 per SM, at most the portable cluster size
-    const int rows = B * Hg;
-    C = (148 * 8 + rows - 1) / rows;
-    C = C < 1 ? 1 : (C > 8 ? 8 : C);
-  }
-  if (C > 8) return IG_EINVAL;
-  const int quads = S_max / 4;
-  const size_t smem = (size_t)((quads + C - 1) / C) * sizeof(float4);
-  if (smem > 200 * 1024) return IG_EINVAL;
-  if (smem > 32 * 1024)  // dynamic + static must fit: opt in early
-    IG_CUDA_STATUS(cudaFuncSetAttribute(rehearse_count_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(C, Hg, B);
-  cfg.blockDim = dim3(kFusedThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = (cudaStream_t)stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  IG_CUDA_STATUS(cudaLaunchKernelEx(&cfg, rehearse_count_kernel, qspec, ldq, cols, pk, st, Hg, d,
-                                    k, S_max, scale, alpha, scores, counts, count_sum));
+  dim3 grid((S_max + kRehearseChunk - 1) / kRehearseChunk, Hg, B);
+  rehearse_count_kernel<<<grid, kRehearseThreads, 0, (cudaStream_t)stream>>>(
+      qspec, ldq, cols, pk, st, Hg, d, k, S_max, scale, alpha, scores, maxkey, tickets, counts,
+      count_sum);
+  IG_LAUNCH_STATUS();
   return IG_OK;
 }
 

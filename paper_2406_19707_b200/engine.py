@@ -257,7 +257,8 @@ class DecodeEngine:
         self.o = torch.empty((B, D), dtype=f32, device=dev)
         self.hidden = torch.empty((B, F), dtype=f32, device=dev)
         self.scores = torch.empty((B, Hg, S), dtype=f32, device=dev)
-        self.maxkey = torch.zeros((L, B, Hg), dtype=i32, device=dev)
+        self.maxkey = torch.zeros((B, Hg), dtype=i32, device=dev)      # rehearse scratch
+        self.rtickets = torch.zeros((B, Hg), dtype=i32, device=dev)    # (left zeroed)
         self.counts = torch.zeros((B, Hg), dtype=i32, device=dev)
         self.count_sum = torch.zeros((L, B), dtype=i32, device=dev)
         self.idx = torch.zeros((L, B, Hg, cap), dtype=i32, device=dev)
@@ -563,7 +564,8 @@ class DecodeEngine:
             self.count_sum[li].zero_()
             _lib.call("ig_rehearse_count", self.qspec.data_ptr(), Hgd, self.cols[li].data_ptr(),
                       self.pk[li - 1].data_ptr(), self.st.data_ptr(), B, Hg, d, kc, S, self.scale,
-                      float(sc.alpha), 0, self.scores.data_ptr(), self.counts.data_ptr(),
+                      float(sc.alpha), self.scores.data_ptr(), self.maxkey.data_ptr(),
+                      self.rtickets.data_ptr(), self.counts.data_ptr(),
                       self.count_sum[li].data_ptr(), h)
 
         idx_tmp = torch.empty_like(self.idx[li])
@@ -649,7 +651,8 @@ class DecodeEngine:
                         _lib.call("ig_rehearse_count", self.qspec.data_ptr(), Hgd,
                                   self.cols[nxt].data_ptr(), self.pk[nxt - 1].data_ptr(),
                                   self.st.data_ptr(), B, Hg, d, self.kcols, self.S_max,
-                                  self.scale, float(sc.alpha), 0, self.scores.data_ptr(),
+                                  self.scale, float(sc.alpha), self.scores.data_ptr(),
+                                  self.maxkey.data_ptr(), self.rtickets.data_ptr(),
                                   self.counts.data_ptr(), self.count_sum[nxt].data_ptr(), cs)
                         self._mark("rehearse", nxt, C, False)
                         self._mark("select", nxt, C, True)

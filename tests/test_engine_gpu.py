@@ -331,3 +331,41 @@ def test_fetch_implementations_identical(impl, ctas, threads, rows):
         finally:
             eng.close()
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("n_rows", [1, 2, 7, 9, 33, 255, 257])
+def test_fast_attention_ragged_groups(n_rows):
+    """Partial 8-row groups and chunk tails in attend512 (d = 128, f16): stale
+    registers of out-of-range rows must not leak (0 * NaN) into the output."""
+    import ctypes
+    import torch
+    from paper_2406_19707_b200 import _lib
+    rng = np.random.default_rng(n_rows)
+    B, Hg, d, cap = 2, 3, 128, 260
+    q = torch.from_numpy(rng.standard_normal((B, 3 * Hg * d)).astype(np.float32)).cuda()
+    stage = torch.full((B, Hg, cap, 2 * d), float("nan"), dtype=torch.float16, device="cuda")
+    stage[:, :, :n_rows] = torch.from_numpy(rng.standard_normal((B, Hg, n_rows, 2 * d)).astype(np.float16)).cuda()
+    n = torch.full((B,), n_rows, dtype=torch.int32, device="cuda")
+    idx = torch.from_numpy(np.tile(np.arange(cap, dtype=np.int32), (B, Hg, 1))).cuda()
+    pos = torch.full((B, Hg), -1, dtype=torch.int32, device="cuda")
+    st = torch.zeros(8, dtype=torch.int32, device="cuda")
+    pf, tk = ctypes.c_size_t(), ctypes.c_size_t()
+    _lib.call("ig_attend_scratch", B, Hg, d, cap, ctypes.byref(pf), ctypes.byref(tk), kernels=0)
+    part = torch.empty(pf.value, device="cuda")
+    tick = torch.zeros(tk.value, dtype=torch.int32, device="cuda")
+    out = torch.empty((B, Hg * d), device="cuda")
+    _lib.call("ig_attend", q.data_ptr(), 3 * Hg * d, q.data_ptr() + 4 * Hg * d, q.data_ptr() + 8 * Hg * d,
+              3 * Hg * d, stage.data_ptr(), _lib.ELT["f16"], idx.data_ptr(), n.data_ptr(), pos.data_ptr(),
+              st.data_ptr(), B, Hg, d, cap, part.data_ptr(), tick.data_ptr(), out.data_ptr(), Hg * d,
+              _lib.stream_handle())
+    o = out.cpu().numpy()
+    assert np.all(np.isfinite(o))
+    qn = q.cpu().numpy().astype(np.float64)
+    st_np = stage[:, :, :n_rows].float().cpu().numpy().astype(np.float64)
+    for b in range(B):
+        for h in range(Hg):
+            K = np.concatenate([st_np[b, h, :, :d], qn[b, Hg * d + h * d:Hg * d + (h + 1) * d][None]])
+            V = np.concatenate([st_np[b, h, :, d:], qn[b, 2 * Hg * d + h * d:2 * Hg * d + (h + 1) * d][None]])
+            lg = K @ qn[b, h * d:(h + 1) * d] / np.sqrt(d)
+            w = np.exp(lg - lg.max())
+            np.testing.assert_allclose(o[b, h * d:(h + 1) * d], (w / w.sum()) @ V, rtol=1e-4, atol=1e-4)
