@@ -62,10 +62,13 @@ def test_layer_pipeline_full_size(name, B, Hg, s):
     scores = torch.empty(B, Hg, S, device=dev)
     counts = torch.zeros(B, Hg, dtype=torch.int32, device=dev)
     csum = torch.zeros(B, dtype=torch.int32, device=dev)
+    mk = torch.zeros((B, Hg), dtype=torch.int32, device=dev)
+    tk0 = torch.zeros((B, Hg), dtype=torch.int32, device=dev)
     scale = float(np.float32(1.0 / np.sqrt(d)))
     _lib.call("ig_rehearse_count", qspec.data_ptr(), Hg * d, cols.data_ptr(), pk.data_ptr(),
-              st.data_ptr(), B, Hg, d, k, S, scale, ALPHA, 0, scores.data_ptr(), counts.data_ptr(),
-              csum.data_ptr(), hs)
+              st.data_ptr(), B, Hg, d, k, S, scale, ALPHA, scores.data_ptr(), mk.data_ptr(),
+              tk0.data_ptr(), counts.data_ptr(), csum.data_ptr(), hs)
+    assert not mk.any() and not tk0.any()      # scratch left zeroed
     qsel = torch.gather(qspec.view(B, Hg, d).double(), 2, cols.long())           # [B, Hg, k]
     ref = torch.einsum("bhj,bhjt->bht", qsel, pk[..., :s].double()) * scale
     sc = scores[..., :s]
