@@ -58,6 +58,7 @@ def _args():
     ap.add_argument("--fetch-priority", type=int, default=0, help="CUDA stream priority (-1 = high)")
     ap.add_argument("--fetch-impl", default="tma", choices=["ldg", "tma"])
     ap.add_argument("--fetch-rows", type=int, default=16, help="TMA rows per warp batch")
+    ap.add_argument("--dense", default="ig", choices=["ig", "cublas"])
     ap.add_argument("--no-hbm-variant", action="store_true",
                     help="skip the secondary run with layer 0's KV resident in HBM")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -199,6 +200,7 @@ def _config(a) -> dict:
             "fetch": (f"{a.fetch_impl} x {a.fetch_ctas} CTAs x {a.fetch_threads} threads"
                       + (f" x {a.fetch_rows} rows/batch" if a.fetch_impl == "tma" else "")),
             "parallelism": f"tp{a.gpus} (heads)" if a.gpus > 1 else "single GPU",
+            "dense": "ig_sgemm_rows (f32)" if a.dense == "ig" else "cuBLAS f32 (TF32 off)",
             "l2": "inputs larger than L2 (partial K >= 1.6 GB streamed per layer set; host pool 54 GB)"}
 
 
@@ -234,7 +236,7 @@ def run_b200(a) -> None:
                     speculation=SpeculationConfig(WORKLOAD["ratio"], WORKLOAD["alpha"], WORKLOAD["cap"], 1))
     eng = DecodeEngine(model, cfg, pool_dtype="f16", device=dev, group=group, fetch_ctas=a.fetch_ctas,
                        fetch_threads=a.fetch_threads, fetch_priority=a.fetch_priority,
-                       fetch_impl=a.fetch_impl, fetch_rows=a.fetch_rows)
+                       fetch_impl=a.fetch_impl, fetch_rows=a.fetch_rows, dense=a.dense)
     # engine holds its own (sharded) copies: drop the full model
     del model
     torch.cuda.empty_cache()
@@ -328,7 +330,7 @@ def run_b200(a) -> None:
                 "bytes_per_launch": f_bytes / max(f_launch, 1),
                 "step_share": f_ms / ms if ms else None}
         hbm = {}
-        for k in ("rehearse_count", "attend", "select"):   # alone: the kernels' own roofline
+        for k in ("rehearse_count", "attend", "select", "dense_ffn_in"):   # alone: own roofline
             if k in iso:
                 gbs = iso[k]["gbs"]
                 hbm[k] = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s",

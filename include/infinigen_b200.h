@@ -181,6 +181,17 @@ int ig_attend(const float* q, int ldq, const float* k_cur, const float* v_cur, i
 int ig_memcpy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
                 size_t height, void* stream);
 
+/* ---- dense projections of the decode step (engine.py:323-327, 360-364) ----
+ * Y[M][N] = X[M][K] . W[K][N] in IEEE f32, M <= 32 (sequences), W row-major;
+ * epilogue 0 = none, 1 = ReLU, 2 = Y = R + X.W (residual).  K split over
+ * `ksplit` CTAs per 128-column tile (ig_sgemm_rows_ksplit suggests one);
+ * workspace >= ceil(N/128) * ksplit * M * 128 floats; tickets >= ceil(N/128)
+ * ints, zeroed once and left zeroed.  Deterministic (fixed reduction order). */
+int ig_sgemm_rows_ksplit(int M, int N, int K);
+int ig_sgemm_rows(const float* X, int ldx, const float* W, int ldw, float* Y, int ldy,
+                  const float* R, int ldr, int M, int N, int K, int ksplit, int epilogue,
+                  float* workspace, size_t workspace_floats, int32_t* tickets, void* stream);
+
 /* ---- step bookkeeping -------------------------------------------------- */
 /* s_len = min(s_len + 1, limit), seq += 2, step += 1 (engine.py:377-378). */
 int ig_step_advance(ig_step_state* st, void* stream);

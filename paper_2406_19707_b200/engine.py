@@ -164,7 +164,7 @@ class DecodeEngine:
     def __init__(self, model, config: RunConfig, *, max_steps: int | None = None,
                  pool_dtype: str = "f16", device=None, group=None, fetch_ctas: int = 32,
                  fetch_threads: int = 32, fetch_priority: int = 0, hbm_layers: int = 0,
-                 fetch_impl: str = "tma", fetch_rows: int = 16):
+                 fetch_impl: str = "tma", fetch_rows: int = 16, dense: str = "ig"):
         config.validate()
         _lib.load()
         _enable_ieee_fp32()
@@ -204,6 +204,9 @@ class DecodeEngine:
             raise ValueError("fetch_impl must be 'ldg' or 'tma'")
         self.fetch_impl = fetch_impl
         self.fetch_rows = fetch_rows
+        if dense not in ("ig", "cublas"):
+            raise ValueError("dense must be 'ig' or 'cublas'")
+        self.dense = dense
         if hbm_layers not in (0, 1) or hbm_layers > spec.layers:
             raise ValueError("hbm_layers must be 0 or 1")
         self.hbm_layers = hbm_layers
@@ -270,6 +273,16 @@ class DecodeEngine:
                            for _ in range(1 if spec_ else 2)]
         self.stage_sel = [torch.empty((B, Hg, cap, 2 * d), dtype=T, device=dev)
                           for _ in range(2 if spec_ else 0)]
+        # skinny-GEMM workspace: the largest ceil(N/128) * ksplit * B * 128 over the projections
+        shapes = [(3 * Hg * d, D), (Hg * d, D), (D, Hg * d), (F, D), (D, F)]   # (N, K)
+        ws = 0
+        self.gemm_ksplit = {}
+        for N_, K_ in shapes:
+            ksp = _lib.load().ig_sgemm_rows_ksplit(B, N_, K_)
+            self.gemm_ksplit[(N_, K_)] = ksp
+            ws = max(ws, ((N_ + 127) // 128) * ksp * B * 128)
+        self.gemm_ws = torch.empty(ws, dtype=f32, device=dev)
+        self.gemm_tickets = torch.zeros(max((N_ + 127) // 128 for N_, _ in shapes), dtype=i32, device=dev)
         pf, tk = ctypes.c_size_t(), ctypes.c_size_t()
         _lib.call("ig_attend_scratch", B, Hg, d, S, ctypes.byref(pf), ctypes.byref(tk), kernels=0)
         self.att_partial = torch.empty(pf.value, dtype=f32, device=dev)
@@ -579,9 +592,15 @@ class DecodeEngine:
         def attend():
             self._attend(li, self.stage_sel[li % 2], self.idx[li], self.n[li], self.cap, h)
 
+        hid = torch.empty_like(self.hidden)
+
+        def ffn_in():
+            self._gemm(self.x_f, self.ffn_in[li], hid, h, epilogue=1)
+
         rows = [("rehearse_count", rehearse, 4 * B * Hg * s * (kc + 1)),
                 ("select", select, 4 * B * Hg * s),
-                ("attend", attend, n_tot * Hg * self.row_bytes)]
+                ("attend", attend, n_tot * Hg * self.row_bytes),
+                ("dense_ffn_in", ffn_in, 4 * (self.D * self.F + B * self.D + B * self.F))]
         out = {}
         for name, fn, nbytes in rows:
             ms = best(fn)
@@ -590,6 +609,24 @@ class DecodeEngine:
         return out
 
     # ----------------------------------------------------------------- decode
+    def _gemm(self, X, W, Y, cs, epilogue: int = 0, R=None) -> None:
+        """Y = X @ W (+ ReLU / + R) on the compute stream."""
+        M, K = X.shape
+        N = W.shape[1]
+        if self.dense == "cublas":
+            if epilogue == 2:
+                torch.addmm(R, X, W, out=Y)
+            else:
+                torch.matmul(X, W, out=Y)
+                if epilogue == 1:
+                    Y.relu_()
+            return
+        ksp = self.gemm_ksplit.get((N, K)) or _lib.load().ig_sgemm_rows_ksplit(M, N, K)
+        _lib.call("ig_sgemm_rows", X.data_ptr(), X.stride(0), W.data_ptr(), W.stride(0),
+                  Y.data_ptr(), Y.stride(0), _lib.ptr(R), R.stride(0) if R is not None else 0,
+                  M, N, K, ksp, epilogue, self.gemm_ws.data_ptr(), self.gemm_ws.numel(),
+                  self.gemm_tickets.data_ptr(), cs)
+
     def _issue_full_fetch(self, li: int, s: int, stage: torch.Tensor) -> None:
         self._mark("fetch", li, self.fetch_stream, True)
         _lib.call("ig_fetch_all", self._pool_layer_host(li), self.B, self.Hg, self.S_max, s,
@@ -646,7 +683,7 @@ class DecodeEngine:
                 nxt = li + 1
                 if nxt < L:
                     if speculative:
-                        torch.matmul(self.x_a, self.wqkv[nxt][:, :Hgd], out=self.qspec)
+                        self._gemm(self.x_a, self.wqkv[nxt][:, :Hgd], self.qspec, cs)
                         self._mark("rehearse", nxt, C, True)
                         _lib.call("ig_rehearse_count", self.qspec.data_ptr(), Hgd,
                                   self.cols[nxt].data_ptr(), self.pk[nxt - 1].data_ptr(),
@@ -689,7 +726,7 @@ class DecodeEngine:
                             Fs.wait_event(self.ev_step)
                         self._issue_full_fetch(nxt, s, self.stage_full[nxt % 2])
                     self.ev_fetch[nxt].record(Fs)
-                torch.matmul(self.x_a, self.wqkv[li], out=self.qkv)
+                self._gemm(self.x_a, self.wqkv[li], self.qkv, cs)
                 sel = speculative and li >= 1
                 _lib.call("ig_append", self.qkv.data_ptr() + 4 * Hgd, self.qkv.data_ptr() + 8 * Hgd,
                           3 * Hgd, self._pool_layer_dev(li), _lib.ELT[self.elt],
@@ -712,16 +749,17 @@ class DecodeEngine:
                     self._attend(li, stage, None, None, self.S_max, cs)
                 self._mark("attend", li, C, False)
                 self.ev_att[li].record(C)
-                torch.matmul(self.attn, self.wo[li], out=self.o)
                 if self.world > 1:
+                    self._gemm(self.attn, self.wo[li], self.o, cs)
                     dist.all_reduce(self.o, group=self.group)
-                self.o.add_(x)                                  # x_mid = x + attn_out
+                    self.o.add_(x)                              # x_mid = x + attn_out
+                else:
+                    self._gemm(self.attn, self.wo[li], self.o, cs, epilogue=2, R=x)
                 _lib.call("ig_layernorm", self.o.data_ptr(), g2.data_ptr(), b2.data_ptr(),
                           float(spec.ln_eps), B, self.D, self.x_f.data_ptr(), cs)
-                torch.matmul(self.x_f, self.ffn_in[li], out=self.hidden)
-                self.hidden.relu_()
+                self._gemm(self.x_f, self.ffn_in[li], self.hidden, cs, epilogue=1)
                 x_new = self.xbuf[1] if x is self.xbuf[0] else self.xbuf[0]
-                torch.addmm(self.o, self.hidden, self.ffn_out[li], out=x_new)
+                self._gemm(self.hidden, self.ffn_out[li], x_new, cs, epilogue=2, R=self.o)
                 if recording:
                     self._record(li, s, recs, spec_scores)
                 x = x_new
