@@ -369,3 +369,34 @@ def test_fast_attention_ragged_groups(n_rows):
             lg = K @ qn[b, h * d:(h + 1) * d] / np.sqrt(d)
             w = np.exp(lg - lg.max())
             np.testing.assert_allclose(o[b, h * d:(h + 1) * d], (w / w.sum()) @ V, rtol=1e-4, atol=1e-4)
+
+
+@pytest.mark.parametrize("policy", ["counter", "lru", "fifo"])
+def test_long_run_eviction_and_saturation(policy):
+    """300 decode steps with a pool limit: rows get fetched > 255 times, so the
+    8-bit counters saturate and every pool halves ("hit 255 -> halve all",
+    pool.py:95-98) many times, and victims churn under each policy.  Every
+    step's selections / events and the final metadata must equal the oracle's."""
+    from paper_2406_19707_b200 import DecodeEngine
+    _, sk = models("m64")
+    ocfg = O.RunConfig(scheme="speculative", prompt_len=24, gen_len=300, batch=1,
+                       pool_limit=20, pool_policy=O.Policy(policy), record_selection=True)
+    sessions = oracle_sessions(sk, ocfg)
+    eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg), copy.deepcopy(sessions), pool_dtype="f32")
+    try:
+        ref_out, ref_recs = oracle_decode(sessions, ocfg.gen_len)
+        got = np.stack([eng.x.cpu().numpy()] + [eng.decode_step().cpu().numpy()
+                                                for _ in range(ocfg.gen_len)], axis=1)
+        assert _scaled_err(got, ref_out) < 1e-3
+        _cmp_records(eng.records, ref_recs, 1, exact=True)
+        halvings = 0
+        for li in range(sk.spec.layers):
+            for h in range(sk.spec.heads):
+                p = sessions[0].pools[li][h]
+                np.testing.assert_array_equal(eng.counter[li, 0, h, :len(p)].cpu().numpy(), p.fetch_counter)
+                np.testing.assert_array_equal(eng.lastf[li, 0, h, :len(p)].cpu().numpy(), p.last_fetch_seq)
+                np.testing.assert_array_equal(eng.arrival[li, 0, h, :len(p)].cpu().numpy(), p.arrival_seq)
+                halvings += int(p.fetch_counter.max() < 255)
+        assert halvings > 0
+    finally:
+        eng.close()
