@@ -144,7 +144,8 @@ def generate_synthetic_gpu(spec: ModelSpec, device="cuda", seed: int | None = No
     return Model(spec, layers, False, picks.cpu().numpy())
 
 
-def skew_model_gpu(model: Model, calib_tokens: int | None = None, seed: int = 0) -> Model:
+def skew_model_gpu(model: Model, calib_tokens: int | None = None, seed: int = 0,
+                   calib_input=None) -> Model:
     """Offline skew (skewing.py:30-104) on the GPU, in place: forward a
     seeded 4*d-row calibration prompt, SVD each head's Q (f64), take A = V with
     the max-|entry|-positive sign rule (skewing.py:59-66), fold A into the
@@ -155,9 +156,12 @@ def skew_model_gpu(model: Model, calib_tokens: int | None = None, seed: int = 0)
     d = spec.head_dim
     n = calib_tokens if calib_tokens is not None else 4 * d
     dev = model.layers[0].w_q.device
-    g = torch.Generator(device=dev)
-    g.manual_seed(seed)
-    x = torch.empty(max(n, 2), spec.model_dim, device=dev).normal_(generator=g)
+    if calib_input is not None:        # e.g. the reference's random_prompt(4d, D, seed)
+        x = calib_input.to(device=dev, dtype=torch.float32)
+    else:
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        x = torch.empty(max(n, 2), spec.model_dim, device=dev).normal_(generator=g)
     for lw in model.layers:
         out, q = _pf.dense_block_forward(x, lw, spec)
         qh = q.view(q.shape[0], spec.heads, d).permute(1, 0, 2).double()  # H x n x d

@@ -400,3 +400,55 @@ def test_long_run_eviction_and_saturation(policy):
         assert halvings > 0
     finally:
         eng.close()
+
+
+def test_gpu_skew_matches_oracle():
+    """skew_model_gpu (torch SVD in f64 + the max-|entry|-positive sign rule,
+    skewing.py:30-95) reproduces the oracle's Jacobi-SVD skew blocks."""
+    import torch
+    from paper_2406_19707_b200.model import LayerWeights, Model, ModelSpec, skew_model_gpu
+    plain, sk = models("m64")
+    sp = plain.spec
+    layers = [LayerWeights(**{f: torch.from_numpy(np.array(getattr(lw, f))).cuda() for f in
+                              ("w_q", "w_k", "w_v", "w_o", "ffn_in", "ffn_out",
+                               "ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias")})
+              for lw in plain.layers]
+    gm = Model(ModelSpec(sp.layers, sp.model_dim, sp.heads, sp.ffn_dim, sp.ln_eps), layers)
+    # the oracle calibrates on random_prompt(4d, D, seed 0); feed the GPU the same rows
+    calib = torch.from_numpy(O.random_prompt(4 * sp.head_dim, sp.model_dim, 0)).cuda()
+    skew_model_gpu(gm, calib_input=calib)
+    for li in range(sp.layers):
+        np.testing.assert_allclose(gm.layers[li].w_q.cpu().numpy(), sk.layers[li].w_q, rtol=1e-4, atol=1e-4)
+        np.testing.assert_allclose(gm.layers[li].w_k.cpu().numpy(), sk.layers[li].w_k, rtol=1e-4, atol=1e-4)
+
+
+def test_engine_trace_equals_oracle_trace():
+    """The engine's schema-v1 trace (engine.py:83-196) equals the oracle run()'s
+    field by field (selected lists compared as sorted lists) for a model loaded
+    from a file the real reference wrote (tests/golden/tiny_skewed.json)."""
+    import os
+    from paper_2406_19707_b200 import RunConfig, SpeculationConfig, run
+    from paper_2406_19707_b200.model import load_model
+    path = os.path.join(os.path.dirname(__file__), "golden", "tiny_skewed.json")
+    m = load_model(path)
+    ocfg = O.RunConfig(scheme="speculative", prompt_len=40, gen_len=5, batch=2, record_selection=True,
+                       pool_limit=42, pool_policy=O.Policy.COUNTER)
+    oracle_model = O.Model(O.ModelSpec(2, 32, 2, 64), [O.Layer(*[np.asarray(getattr(lw, f)) for f in
+                           ("w_q", "w_k", "w_v", "w_o", "ffn_in", "ffn_out", "ln1_gain", "ln1_bias",
+                            "ln2_gain", "ln2_bias")]) for lw in m.layers], np.zeros(0, np.int64), True)
+    ref_trace, ref_out = O.run(oracle_model, ocfg)
+    trace, out = run(m, engine_cfg(ocfg), pool_dtype="f32")
+    assert _scaled_err(np.stack(out), np.stack(ref_out)) < 1e-4
+    assert trace["version"] == ref_trace["version"] and trace["layers"] == ref_trace["layers"]
+    assert trace["heads"] == ref_trace["heads"] and trace["head_dim"] == ref_trace["head_dim"]
+    for k, v in ref_trace["config"].items():
+        assert trace["config"][k] == v, k
+    for sm, sr in zip(trace["sequences"], ref_trace["sequences"]):
+        assert sm["prefill"] == sr["prefill"]
+        for itm, itr in zip(sm["iterations"], sr["iterations"]):
+            for rm, rr in zip(itm, itr):
+                for key in ("iteration", "layer", "n_selected", "bytes", "full_bytes", "pool_events"):
+                    assert rm[key] == rr[key], key
+                for key in ("attention_flops", "ffn_flops", "speculation_flops"):
+                    assert rm[key] == pytest.approx(rr[key]), key
+                assert [sorted(x) for x in rm["selected"]] == [sorted(x) for x in rr["selected"]]

@@ -156,3 +156,21 @@ def test_pool_spec_examples():
     q.fetch([0, 2])
     q.fetch([1])
     assert q.evict_select() == 0
+
+
+def test_load_model_reads_reference_files():
+    """paper_2406_19707_b200.load_model reads the reference's manifest + payload
+    format (model.py:284-409) written by the real reference's save_model, and
+    the oracle rebuilds the same weights bit-for-bit."""
+    import os
+    from paper_2406_19707_b200.model import load_model
+    path = os.path.join(os.path.dirname(__file__), "golden", "tiny_skewed.json")
+    m = load_model(path)
+    assert m.skewed and m.spec.layers == 2 and m.spec.model_dim == 32 and m.spec.head_dim == 16
+    spec = O.ModelSpec(layers=2, model_dim=32, heads=2, ffn_dim=64, outlier_channels=4,
+                       outlier_scale=2.0, seed=5)
+    ref = O.skew_model(O.generate_synthetic(spec), calib_seed=1)
+    for li in range(2):
+        for f in ("w_q", "w_k", "w_v", "w_o", "ffn_in", "ffn_out", "ln1_gain", "ln2_bias"):
+            np.testing.assert_allclose(getattr(m.layers[li], f), getattr(ref.layers[li], f),
+                                       rtol=0, atol=1e-6)
