@@ -7,6 +7,8 @@
 // of a (b, h) to arrive (ticket) merges the chunks in fixed chunk order, so the
 // result is deterministic.  Scores are (q . k) / float32(sqrt(d)) -- a division,
 // as in model.py:174 -- and exp is the full-precision expf.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace ig {
@@ -361,6 +363,216 @@ attend512_kernel(const float* __restrict__ q, int ldq, const float* __restrict__
   if (threadIdx.x == 0) tickets[bh] = 0;
 }
 
+// TMA-fed variant of the 512-B-row path: the rows of a (b, h) chunk are
+// contiguous in the stage buffer, so thread 0 streams them into a 4-stage
+// shared-memory ring with one cp.async.bulk of up to 32 rows (16 KB) per stage
+// (mbarrier complete_tx); each warp folds 8 of a stage's rows into its online
+// softmax from shared memory.  Bytes in flight (48 KB per CTA) no longer cost
+// registers, which bounded the register-fed loop at ~0.44 of HBM.
+constexpr int kTmaRows = 32;      // rows per stage (one bulk copy)
+constexpr int kTmaStages = 4;
+constexpr int kTmaChunk = 512;    // rows per CTA
+
+__device__ __forceinline__ void att_mbar_init(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+}
+__device__ __forceinline__ void att_mbar_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void att_mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W_%=;\n}" ::"r"(bar), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void att_bulk(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kAttThreads)
+attend512_tma_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_cur,
+                     const float* __restrict__ v_cur, int ldkv, const T* __restrict__ stage,
+                     const int32_t* __restrict__ idx, const int32_t* __restrict__ n_in,
+                     const int32_t* __restrict__ pos_in, const ig_step_state* __restrict__ st,
+                     int Hg, int cap, float sqrt_d, int max_chunks, float* __restrict__ partial,
+                     int32_t* __restrict__ tickets, float* __restrict__ out, int ldo) {
+  constexpr int d = 128;
+  extern __shared__ __align__(128) uint4 ring[];          // [kTmaStages][kTmaRows][32]
+  __shared__ __align__(8) unsigned long long bars[kTmaStages];
+  const int b = blockIdx.z, h = blockIdx.y, c = blockIdx.x;
+  const size_t bh = (size_t)b * Hg + h;
+  const int rows = n_in ? n_in[b] : st->s_len;
+  const int nchunks = max(1, (rows + kTmaChunk - 1) / kTmaChunk);
+  if (c >= nchunks) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool klane = lane < 16;
+  const int e0 = (lane & 15) * 8;
+  const int pos = pos_in[bh];
+  const int r0 = c * kTmaChunk, r1 = min(rows, r0 + kTmaChunk);
+  const int nst = (r1 - r0 + kTmaRows - 1) / kTmaRows;   // stages of this chunk (may be 0)
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(stage + bh * (size_t)cap * 2 * d);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTmaStages; ++i) att_mbar_init((uint32_t)__cvta_generic_to_shared(&bars[i]));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int j) {       // thread 0: stage j of this chunk -> ring slot j % kTmaStages
+    const int rs = r0 + j * kTmaRows, cnt = min(kTmaRows, r1 - rs);
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&bars[j % kTmaStages]);
+    att_mbar_expect(bar, (uint32_t)cnt * 512u);
+    att_bulk((uint32_t)__cvta_generic_to_shared(ring + (size_t)(j % kTmaStages) * kTmaRows * 32),
+             src + (size_t)rs * 512, (uint32_t)cnt * 512u, bar);
+  };
+  if (threadIdx.x == 0)
+    for (int j = 0; j < min(nst, kTmaStages); ++j) issue(j);
+
+  float qv[8];
+  {
+    const float* qr = q + (size_t)b * ldq + (size_t)h * d + e0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) qv[i] = klane ? qr[i] : 0.f;
+  }
+  float m = -INFINITY, l = 0.f, acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+
+  for (int j = 0; j < nst; ++j) {
+    const int rb = r0 + j * kTmaRows + w * 8;             // my 8 rows of this stage
+    int rowid = 0;
+    if (idx && lane < 8 && rb + lane < r1) rowid = idx[bh * cap + rb + lane];
+    att_mbar_wait((uint32_t)__cvta_generic_to_shared(&bars[j % kTmaStages]), (j / kTmaStages) & 1);
+    const uint4* sl = ring + (size_t)(j % kTmaStages) * kTmaRows * 32 + (size_t)(w * 8) * 32;
+    float dot[8];
+    uint4 raw[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      raw[u] = rb + u < r1 ? sl[u * 32 + lane] : make_uint4(0u, 0u, 0u, 0u);
+      float f[8];
+      unpack8<T>(raw[u], f);
+      float a = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a = fmaf(qv[i], f[i], a);
+      dot[u] = klane ? a : 0.f;
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], o);
+    }
+    float gm = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int id = idx ? __shfl_sync(0xffffffffu, rowid, u) : rb + u;
+      const bool ok = rb + u < r1 && id != pos;
+      dot[u] = ok ? __shfl_sync(0xffffffffu, dot[u], 0) / sqrt_d : -INFINITY;
+      gm = fmaxf(gm, dot[u]);
+    }
+    if (gm != -INFINITY) {
+      const float mn = fmaxf(m, gm);
+      const float corr = expf(m - mn);
+      float psum = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] *= corr;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float p = expf(dot[u] - mn);
+        psum += p;
+        float f[8];
+        unpack8<T>(raw[u], f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fmaf(p, f[i], acc[i]);
+      }
+      l = l * corr + psum;
+      m = mn;
+    }
+    __syncthreads();                                        // ring slot j % S fully read
+    if (threadIdx.x == 0 && j + kTmaStages < nst) issue(j + kTmaStages);
+  }
+  if (c == 0 && w == 0) {  // the current token: GPU-resident f32 row
+    const float* srcr = (klane ? k_cur : v_cur) + (size_t)b * ldkv + (size_t)h * d + e0;
+    float f[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) f[i] = srcr[i];
+    float dot = 0.f;
+    if (klane) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dot = fmaf(qv[i], f[i], dot);
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    const float sc = __shfl_sync(0xffffffffu, dot, 0) / sqrt_d;
+    const float mn = fmaxf(m, sc);
+    const float corr = expf(m - mn);
+    const float p = expf(sc - mn);
+    l = l * corr + p;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = fmaf(p, f[i], acc[i] * corr);
+    m = mn;
+  }
+
+  __shared__ float wm[kAttWarps], wl[kAttWarps];
+  __shared__ float wacc[kAttWarps][d];
+  if (lane == 0) { wm[w] = m; wl[w] = l; }
+  if (!klane) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) wacc[w][e0 + i] = acc[i];
+  }
+  __syncthreads();
+  float M = -INFINITY;
+  for (int i = 0; i < kAttWarps; ++i) M = fmaxf(M, wm[i]);
+  float* part = partial + (bh * max_chunks + c) * (size_t)(d + 2);
+  if (threadIdx.x == 0) {
+    float L = 0.f;
+    for (int i = 0; i < kAttWarps; ++i) L += wl[i] * (wm[i] == -INFINITY ? 0.f : expf(wm[i] - M));
+    part[0] = M;
+    part[1] = L;
+  }
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    float a = 0.f;
+    for (int i = 0; i < kAttWarps; ++i) a += wacc[i][e] * (wm[i] == -INFINITY ? 0.f : expf(wm[i] - M));
+    part[2 + e] = a;
+  }
+  __shared__ int last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(tickets + bh, 1) == nchunks - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const float* pb = partial + bh * max_chunks * (size_t)(d + 2);
+  float MM = -INFINITY;
+  for (int i = 0; i < nchunks; ++i) MM = fmaxf(MM, __ldcg(pb + (size_t)i * (d + 2)));
+  float LL = 0.f;
+  for (int i = 0; i < nchunks; ++i) {
+    const float mi = __ldcg(pb + (size_t)i * (d + 2));
+    LL += __ldcg(pb + (size_t)i * (d + 2) + 1) * (mi == -INFINITY ? 0.f : expf(mi - MM));
+  }
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    float a = 0.f;
+    for (int i = 0; i < nchunks; ++i) {
+      const float mi = __ldcg(pb + (size_t)i * (d + 2));
+      a += __ldcg(pb + (size_t)i * (d + 2) + 2 + e) * (mi == -INFINITY ? 0.f : expf(mi - MM));
+    }
+    out[(size_t)b * ldo + (size_t)h * d + e] = a / LL;
+  }
+  if (threadIdx.x == 0) tickets[bh] = 0;
+}
+
+// IG_ATTEND_IMPL=tma selects the TMA-fed 512-B path.  Measured alone at C3
+// (round 1): register-fed 2.84 TB/s vs TMA-fed 2.39 TB/s -- the per-row math
+// (f16 unpack + shuffle reductions), not the feed, bounds this kernel, so
+// the register-fed loop stays the default.
+inline bool attend_tma_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("IG_ATTEND_IMPL");
+    return v && v[0] == 't';
+  }();
+  return on;
+}
+
 template <typename T>
 int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const float* k_cur,
                   const float* v_cur, int ldkv, const void* stage, const int32_t* idx,
@@ -368,7 +580,18 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
                   int cap, float sqrt_d, int max_chunks, float* partial, int32_t* tickets,
                   float* out, int ldo) {
   if constexpr (sizeof(T) == 2) {
-    if (d == 128) {  // 512-B rows: the production shape
+    if (d == 128 && attend_tma_enabled()) {  // 512-B rows, TMA-fed (opt-in)
+      const int mc = (cap + kTmaChunk - 1) / kTmaChunk;
+      const size_t smem = (size_t)kTmaStages * kTmaRows * 512;
+      IG_CUDA_STATUS(cudaFuncSetAttribute(attend512_tma_kernel<T>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attend512_tma_kernel<T><<<dim3(mc, grid.y, grid.z), kAttThreads, smem, s>>>(
+          q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, pos, st, Hg, cap, sqrt_d,
+          max_chunks, partial, tickets, out, ldo);
+      IG_LAUNCH_STATUS();
+      return IG_OK;
+    }
+    if (d == 128) {  // 512-B rows, register-fed (default)
       const int mc = (cap + kFastChunk - 1) / kFastChunk;
       attend512_kernel<T><<<dim3(mc, grid.y, grid.z), kAttThreads, 0, s>>>(
           q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, pos, st, Hg, cap, sqrt_d,

@@ -255,3 +255,40 @@ def test_sgemm_rows_vs_float64(M, N, K, epilogue):
     torch.testing.assert_close(outs[0].double(), ref, rtol=1e-5, atol=2e-4 * max(1.0, K ** 0.5 / 8))
     assert torch.equal(outs[0], outs[1])
     assert not tk.any()
+
+
+def test_attend_tma_variant_matches(monkeypatch):
+    """The opt-in TMA-fed attention (IG_ATTEND_IMPL=tma) runs in a subprocess
+    (the switch is read once per process) and must equal the default path."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, ctypes\n"
+        "from paper_2406_19707_b200 import _lib\n"
+        "rng = np.random.default_rng(3)\n"
+        "B, Hg, d, cap = 2, 3, 128, 700\n"
+        "q = torch.from_numpy(rng.standard_normal((B, 3*Hg*d)).astype(np.float32)).cuda()\n"
+        "stage = torch.from_numpy(rng.standard_normal((B, Hg, cap, 2*d)).astype(np.float16)).cuda()\n"
+        "n = torch.tensor([700, 37], dtype=torch.int32, device='cuda')\n"
+        "idx = torch.from_numpy(np.tile(np.arange(cap, dtype=np.int32), (B, Hg, 1))).cuda()\n"
+        "pos = torch.full((B, Hg), 5, dtype=torch.int32, device='cuda')\n"
+        "st = torch.zeros(8, dtype=torch.int32, device='cuda')\n"
+        "pf, tk = ctypes.c_size_t(), ctypes.c_size_t()\n"
+        "_lib.call('ig_attend_scratch', B, Hg, d, cap, ctypes.byref(pf), ctypes.byref(tk), kernels=0)\n"
+        "part = torch.empty(pf.value, device='cuda'); tick = torch.zeros(tk.value, dtype=torch.int32, device='cuda')\n"
+        "out = torch.empty((B, Hg*d), device='cuda')\n"
+        "_lib.call('ig_attend', q.data_ptr(), 3*Hg*d, q.data_ptr()+4*Hg*d, q.data_ptr()+8*Hg*d, 3*Hg*d, stage.data_ptr(),"
+        " _lib.ELT['f16'], idx.data_ptr(), n.data_ptr(), pos.data_ptr(), st.data_ptr(), B, Hg, d, cap, part.data_ptr(),"
+        " tick.data_ptr(), out.data_ptr(), Hg*d, _lib.stream_handle())\n"
+        "np.save(__import__('sys').argv[1], out.cpu().numpy())\n")
+    import os
+    import tempfile
+    outs = []
+    for impl in ("ldg", "tma"):
+        f = os.path.join(tempfile.mkdtemp(), "o.npy")
+        env = dict(os.environ, IG_ATTEND_IMPL=impl)
+        r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True,
+                           cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    np.testing.assert_allclose(outs[0], outs[1], rtol=1e-5, atol=1e-6)
