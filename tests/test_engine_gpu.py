@@ -452,3 +452,42 @@ def test_engine_trace_equals_oracle_trace():
                 for key in ("attention_flops", "ffn_flops", "speculation_flops"):
                     assert rm[key] == pytest.approx(rr[key]), key
                 assert [sorted(x) for x in rm["selected"]] == [sorted(x) for x in rr["selected"]]
+
+
+@pytest.mark.slow
+def test_c1_opt125m_shape_end_to_end():
+    """BASELINE.json configs[0]: OPT-125M shape (12 x 768, 12 heads, d 64),
+    2048-token prompt, alpha 4, ratio 0.3.  The oracle skews and prefills (the
+    reference's own CPU path), the B200 engine (f32 pool) then decodes 12
+    steps free-running next to the oracle.  Selections must agree on >= 99.9%
+    of the ~1.6 K (step, layer, head) sets -- any disagreement must be a near
+    tie at the top-n boundary -- and outputs within 1e-3 scaled."""
+    from paper_2406_19707_b200 import DecodeEngine
+    spec = O.ModelSpec(layers=12, model_dim=768, heads=12, ffn_dim=3072, outlier_channels=8,
+                       outlier_scale=2.0, seed=0)
+    model = O.skew_model(O.generate_synthetic(spec), calib_seed=0)
+    ocfg = O.RunConfig(scheme="speculative", prompt_len=2048, gen_len=12, batch=1,
+                       record_selection=True, record_scores=True)
+    sessions = oracle_sessions(model, ocfg)
+    eng = DecodeEngine.from_sessions(model, engine_cfg(ocfg, record_scores=True),
+                                     copy.deepcopy(sessions), pool_dtype="f32")
+    try:
+        ref_out, ref_recs = oracle_decode(sessions, ocfg.gen_len)
+        got = np.stack([eng.x.cpu().numpy()] + [eng.decode_step().cpu().numpy()
+                                                for _ in range(ocfg.gen_len)], axis=1)
+        assert _scaled_err(got, ref_out) < 1e-3
+        agree = _cmp_records(eng.records, ref_recs, 1, exact=False)
+        assert agree >= 0.999, agree
+        # every mismatch is a near tie of the (reference) speculated scores
+        for it, per_b in enumerate(eng.records):
+            for li, r in enumerate(per_b[0]):
+                rr = ref_recs[0][it][li]
+                assert r["n_selected"] == rr["n_selected"]
+                for h, (a, c) in enumerate(zip(r["selected"], rr["selected"])):
+                    diff = set(a) ^ set(c)
+                    if diff and "spec_scores" in rr:
+                        v = np.asarray(rr["spec_scores"][h])
+                        kth = np.sort(v)[::-1][rr["n_selected"] - 1]
+                        assert all(abs(v[i] - kth) < 1e-4 * max(1.0, abs(kth)) for i in diff)
+    finally:
+        eng.close()
