@@ -59,6 +59,8 @@ def _args():
     ap.add_argument("--fetch-impl", default="tma", choices=["ldg", "tma"])
     ap.add_argument("--fetch-rows", type=int, default=16, help="TMA rows per warp batch")
     ap.add_argument("--dense", default="ig", choices=["ig", "cublas"])
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo lets N ranks share one GPU (tests of the N > 1 path)")
     ap.add_argument("--no-hbm-variant", action="store_true",
                     help="skip the secondary run with layer 0's KV resident in HBM")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -217,11 +219,15 @@ def run_b200(a) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % torch.cuda.device_count()          # N ranks may share a GPU (gloo tests)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if a.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
         group = dist.group.WORLD
     sh = dict(SHAPES[a.shape])
     if a.layers:
