@@ -127,10 +127,12 @@ int ig_fetch(const void* pool_dev, const int32_t* idx, const int32_t* n, int B, 
  * per CTA; each warp moves `rows_per_batch` (<= 32) rows per batch, one per
  * lane, with two batches loading while the previous one drains (shared memory
  * warps * 3 * rows_per_batch * row_bytes).  The bytes in flight live in shared
- * memory, so the gather takes almost no threads/registers from compute.     */
-int ig_fetch_tma(const void* pool_dev, const int32_t* idx, const int32_t* n, int B, int Hg,
-                 int S_max, int cap, int row_bytes, void* stage, int ctas, int warps,
-                 int rows_per_batch, void* stream);
+ * memory, so the gather takes almost no threads/registers from compute.
+ * idx == NULL: every row [0, st->s_len) of every (b, h) (a full layer whose
+ * size is read on the device -- CUDA-graph capturable; st unused otherwise). */
+int ig_fetch_tma(const void* pool_dev, const int32_t* idx, const int32_t* n,
+                 const ig_step_state* st, int B, int Hg, int S_max, int cap, int row_bytes,
+                 void* stage, int ctas, int warps, int rows_per_batch, void* stream);
 /* Layer 0 (engine.py:393-396): every row [0, s) by copy engine, host sizes. */
 int ig_fetch_all(const void* pool_host, int B, int Hg, int S_max, int s, int row_bytes,
                  void* stage, int stage_rows, void* stream);

@@ -38,7 +38,7 @@ _SIGS = {
     "ig_order_by_score": [_P, _P, _I, _I, _I, _I, _P, _P],
     "ig_topk_rows": [_P, _I, _I, _I, _P, _P],
     "ig_fetch": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P],
-    "ig_fetch_tma": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _I, _I, _P],
+    "ig_fetch_tma": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _I, _I, _P],
     "ig_fetch_all": [_P, _I, _I, _I, _I, _I, _P, _I, _P],
     "ig_append": [_P, _P, _I, _P, _I, _P, _P, _I, _P, _P, _P, _I, _I, _P, _P, _I, _P, _I, _I,
                   _I, _I, _P, _P, _P],

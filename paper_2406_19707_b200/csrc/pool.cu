@@ -119,18 +119,22 @@ constexpr int kTmaBufs = 3;   // batch j loads while j-1 drains; j-2's store rea
 
 __global__ void __launch_bounds__(128)
 fetch_tma_kernel(const uint8_t* __restrict__ pool, const int32_t* __restrict__ idx,
-                 const int32_t* __restrict__ n_in, int B, int Hg, int S_max, int cap, int row_bytes,
-                 int rows_per_batch, uint8_t* __restrict__ stage) {
+                 const int32_t* __restrict__ n_in, const ig_step_state* __restrict__ st, int B,
+                 int Hg, int S_max, int cap, int row_bytes, int rows_per_batch,
+                 uint8_t* __restrict__ stage) {
   const int R = rows_per_batch;   // lanes [0, R) each move one row per batch
+  // idx == nullptr: every row [0, st->s_len) of every (b, h), identity order
+  // (a full layer, graph-capturable: the row count is read on the device)
   extern __shared__ __align__(128) uint8_t tma_smem[];
   __shared__ long long off[kMaxBatch + 1];
   __shared__ __align__(8) unsigned long long bars[4][kTmaBufs];   // <= 4 warps
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (threadIdx.x == 0) {
     long long acc = 0;
+    const int all = idx == nullptr ? st->s_len : 0;
     for (int b = 0; b < B; ++b) {
       off[b] = acc;
-      acc += (long long)n_in[b] * Hg;
+      acc += (long long)(idx == nullptr ? all : n_in[b]) * Hg;
     }
     off[B] = acc;
   }
@@ -163,12 +167,12 @@ fetch_tma_kernel(const uint8_t* __restrict__ pool, const int32_t* __restrict__ i
       if (mine) {
         int b = 0;
         while (off[b + 1] <= g) ++b;
-        const int nb = n_in[b];
         const long long rem = g - off[b];
+        const int nb = (int)((off[b + 1] - off[b]) / Hg);
         const int h = (int)(rem / nb);
         const int r = (int)(rem - (long long)h * nb);
         const size_t bh = (size_t)b * Hg + h;
-        src = pool + (bh * S_max + idx[bh * cap + r]) * (size_t)row_bytes;
+        src = pool + (bh * S_max + (idx ? idx[bh * cap + r] : r)) * (size_t)row_bytes;
         dst = (bh * cap + r) * (size_t)row_bytes;
       }
       const int cnt = __popc(__ballot_sync(0xffffffffu, mine));
@@ -426,11 +430,12 @@ extern "C" int ig_fetch(const void* pool_dev, const int32_t* idx, const int32_t*
   return IG_OK;
 }
 
-extern "C" int ig_fetch_tma(const void* pool_dev, const int32_t* idx, const int32_t* n, int B,
-                            int Hg, int S_max, int cap, int row_bytes, void* stage, int ctas,
-                            int warps, int rows_per_batch, void* stream) {
+extern "C" int ig_fetch_tma(const void* pool_dev, const int32_t* idx, const int32_t* n,
+                            const ig_step_state* st, int B, int Hg, int S_max, int cap,
+                            int row_bytes, void* stage, int ctas, int warps, int rows_per_batch,
+                            void* stream) {
   using namespace ig;
-  if (!pool_dev || !idx || !n || !stage || B < 1 || B > kMaxBatch || Hg < 1 || cap < 1 ||
+  if (!pool_dev || (idx && !n) || (!idx && !st) || !stage || B < 1 || B > kMaxBatch || Hg < 1 || cap < 1 ||
       S_max < 1 || row_bytes < 16 || (row_bytes & 15) || ctas < 1 || warps < 1 || warps > 4 ||
       rows_per_batch < 1 || rows_per_batch > 32)
     return IG_EINVAL;
@@ -440,7 +445,7 @@ extern "C" int ig_fetch_tma(const void* pool_dev, const int32_t* idx, const int3
     IG_CUDA_STATUS(cudaFuncSetAttribute(fetch_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
   fetch_tma_kernel<<<ctas, 32 * warps, smem, (cudaStream_t)stream>>>(
-      (const uint8_t*)pool_dev, idx, n, B, Hg, S_max, cap, row_bytes, rows_per_batch,
+      (const uint8_t*)pool_dev, idx, n, st, B, Hg, S_max, cap, row_bytes, rows_per_batch,
       (uint8_t*)stage);
   IG_LAUNCH_STATUS();
   return IG_OK;

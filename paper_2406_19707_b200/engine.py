@@ -164,7 +164,8 @@ class DecodeEngine:
     def __init__(self, model, config: RunConfig, *, max_steps: int | None = None,
                  pool_dtype: str = "f16", device=None, group=None, fetch_ctas: int = 32,
                  fetch_threads: int = 32, fetch_priority: int = 0, hbm_layers: int = 0,
-                 fetch_impl: str = "tma", fetch_rows: int = 16, dense: str = "ig"):
+                 fetch_impl: str = "tma", fetch_rows: int = 16, dense: str = "ig",
+                 cuda_graph: bool = False):
         config.validate()
         _lib.load()
         _enable_ieee_fp32()
@@ -207,6 +208,14 @@ class DecodeEngine:
         if dense not in ("ig", "cublas"):
             raise ValueError("dense must be 'ig' or 'cublas'")
         self.dense = dense
+        self.cuda_graph = cuda_graph
+        if cuda_graph and (config.record_selection or config.record_scores):
+            raise ValueError("cuda_graph cannot record traces (host reads every layer)")
+        if cuda_graph and group is not None and dist.get_backend(group) != "nccl":
+            raise ValueError("cuda_graph needs NCCL for the collectives")
+        self._graph = None
+        self._graph_mode = False
+        self.graph_launches = 0
         if hbm_layers not in (0, 1) or hbm_layers > spec.layers:
             raise ValueError("hbm_layers must be 0 or 1")
         self.hbm_layers = hbm_layers
@@ -337,6 +346,7 @@ class DecodeEngine:
             self.pool_hbm = None
         self.hbm_layers = n
         self._prefetched0 = False
+        self._graph = None
 
     def _pool_layer_dev(self, li: int) -> int:
         """Device address of layer li's rows (HBM tier or the host pool alias)."""
@@ -406,6 +416,7 @@ class DecodeEngine:
         self.x.copy_(_f32(x, self.device).reshape(self.B, self.D))
         self._set_state(s_len, seq0)
         self._prefetched0 = False
+        self._graph = None
         torch.cuda.synchronize(self.device)
 
     @classmethod
@@ -484,6 +495,7 @@ class DecodeEngine:
         self.counter[..., :rows] = torch.from_numpy(ct).to(self.device)
         self._set_state(rows, N)
         self._prefetched0 = False
+        self._graph = None
         self.prefill_info = {"prompt_len": N, "pool_rows": rows,
                              "partial_cols": self.kcols if (self.scheme == "speculative" and L > 1) else None,
                              "pool_overwrites": ovw * L * self.H}
@@ -500,7 +512,7 @@ class DecodeEngine:
 
     def _mark(self, kind: str, li: int, stream, start: bool):
         inst = self._inst
-        if inst is None or inst["k"] >= inst["steps"]:
+        if inst is None or self._graph_mode or inst["k"] >= inst["steps"]:
             return
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(stream)
@@ -634,6 +646,13 @@ class DecodeEngine:
                   self.fetch_stream.cuda_stream, kernels=0)
         self._mark("fetch", li, self.fetch_stream, False)
 
+    def _issue_full_fetch_dev(self, li: int, stage: torch.Tensor) -> None:
+        """Every row [0, st.s_len) of layer li by the TMA gather (graph mode)."""
+        _lib.call("ig_fetch_tma", self._pool_layer_dev(li), None, None, self.st.data_ptr(), self.B,
+                  self.Hg, self.S_max, self.S_max, self.row_bytes, stage.data_ptr(),
+                  self.fetch_ctas, max(1, self.fetch_threads // 32), self.fetch_rows,
+                  self.fetch_stream.cuda_stream)
+
     def _attend(self, li: int, stage, idx, n, stage_rows: int, cs: int) -> None:
         Hgd = self.Hg * self.d
         q = self.qkv
@@ -654,6 +673,35 @@ class DecodeEngine:
             # construction (prompt_len + max_steps rows) and must not overrun
             raise ValueError(f"pool capacity {self.S_max} rows exhausted after "
                              f"{self.iteration} steps: build the engine with a larger max_steps")
+        if not self.cuda_graph:
+            return self._step()
+        cur = torch.cuda.current_stream(self.device)
+        if self._graph is None:
+            self._graph_mode = True
+            try:
+                l0 = _lib.launches
+                out = self._step()                      # eager step: warms the allocator
+                self.graph_launches = _lib.launches - l0
+                torch.cuda.synchronize(self.device)
+                g = torch.cuda.CUDAGraph()
+                s_keep, it_keep = self.s_host, self.iteration
+                with torch.cuda.graph(g, stream=self.compute):
+                    self._step()                        # captured, not executed
+                self.s_host, self.iteration = s_keep, it_keep
+                self._graph = g
+            finally:
+                self._graph_mode = False
+            return out
+        self.compute.wait_stream(cur)
+        with torch.cuda.stream(self.compute):
+            self._graph.replay()
+        cur.wait_stream(self.compute)
+        lim = self.config.pool_limit
+        self.s_host = min(self.s_host + 1, lim) if lim else self.s_host + 1
+        self.iteration += 1
+        return self.xbuf[0]
+
+    def _step(self) -> torch.Tensor:
         cfg, spec = self.config, self.spec
         L, B, Hg, d = self.L, self.B, self.Hg, self.d
         Hgd = Hg * d
@@ -662,7 +710,8 @@ class DecodeEngine:
         C, Fs = self.compute, self.fetch_stream
         cs = C.cuda_stream
         s = self.s_host
-        recording = cfg.record_selection or cfg.record_scores
+        graph = self._graph_mode
+        recording = (cfg.record_selection or cfg.record_scores) and not graph
         recs = [[None] * L for _ in range(B)]
         spec_scores = [None] * L
         C.wait_stream(torch.cuda.current_stream(self.device))
@@ -671,6 +720,10 @@ class DecodeEngine:
             self.ev_step.record(C)
             if self.hbm_layers:
                 self.ev_fetch[0].record(C)          # layer 0 is HBM-resident: no fetch
+            elif graph:                             # in-step, row count read on the device
+                Fs.wait_event(self.ev_step)
+                self._issue_full_fetch_dev(0, self.stage_full[0])
+                self.ev_fetch[0].record(Fs)
             elif not self._prefetched0:
                 Fs.wait_event(self.ev_step)
                 self._issue_full_fetch(0, s, self.stage_full[0])
@@ -708,8 +761,8 @@ class DecodeEngine:
                         self._mark("fetch", nxt, Fs, True)
                         if self.fetch_impl == "tma":
                             _lib.call("ig_fetch_tma", self._pool_layer_dev(nxt),
-                                      self.idx[nxt].data_ptr(), self.n[nxt].data_ptr(), B, Hg,
-                                      self.S_max, self.cap, self.row_bytes,
+                                      self.idx[nxt].data_ptr(), self.n[nxt].data_ptr(), None, B,
+                                      Hg, self.S_max, self.cap, self.row_bytes,
                                       self.stage_sel[nxt % 2].data_ptr(), self.fetch_ctas,
                                       max(1, self.fetch_threads // 32), self.fetch_rows,
                                       Fs.cuda_stream)
@@ -724,7 +777,10 @@ class DecodeEngine:
                             Fs.wait_event(self.ev_att[li - 1])
                         else:
                             Fs.wait_event(self.ev_step)
-                        self._issue_full_fetch(nxt, s, self.stage_full[nxt % 2])
+                        if graph:
+                            self._issue_full_fetch_dev(nxt, self.stage_full[nxt % 2])
+                        else:
+                            self._issue_full_fetch(nxt, s, self.stage_full[nxt % 2])
                     self.ev_fetch[nxt].record(Fs)
                 self._gemm(self.x_a, self.wqkv[li], self.qkv, cs)
                 sel = speculative and li >= 1
@@ -765,14 +821,18 @@ class DecodeEngine:
                 x = x_new
             _lib.call("ig_step_advance", self.st.data_ptr(), cs)
             inst = self._inst
-            if inst is not None and inst["k"] < inst["steps"]:
+            if inst is not None and not graph and inst["k"] < inst["steps"]:
                 inst["n"][inst["k"]].copy_(self.n)
                 inst["s"].append(s)
                 inst["k"] += 1
             s_next = min(s + 1, cfg.pool_limit) if cfg.pool_limit else s + 1
             # next step's layer-0 rows stream in while the tail of this step runs
             # (after the last attend that reads stage_full[0])
-            if not self.hbm_layers:
+            if graph:
+                if x is not self.xbuf[0]:           # replays must start from xbuf[0]
+                    self.xbuf[0].copy_(x)
+                    x = self.xbuf[0]
+            elif not self.hbm_layers:
                 last0 = 0 if speculative else (L - 1 if (L - 1) % 2 == 0 else L - 2)
                 Fs.wait_event(self.ev_att[last0])
                 self._issue_full_fetch(0, s_next, self.stage_full[0])

@@ -491,3 +491,27 @@ def test_c1_opt125m_shape_end_to_end():
                         assert all(abs(v[i] - kth) < 1e-4 * max(1.0, abs(kth)) for i in diff)
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("rname,pool", [("spec", "f32"), ("spec_counter", "f16"), ("full", "f32")])
+def test_cuda_graph_replay_is_identical(rname, pool):
+    """cuda_graph=True (one eager step, then a captured step replayed) gives the
+    same outputs bit for bit as eager decoding, and leaves the same pool state."""
+    from paper_2406_19707_b200 import DecodeEngine
+    plain, sk = models("m256")
+    ocfg = run_config(rname, gen_len=6)
+    model = sk if ocfg.scheme == "speculative" else plain
+    sessions = oracle_sessions(model, ocfg)
+    outs, meta = [], []
+    for graph in (False, True):
+        eng = DecodeEngine.from_sessions(model, engine_cfg(ocfg, record_selection=False),
+                                         copy.deepcopy(sessions), pool_dtype=pool, cuda_graph=graph)
+        try:
+            outs.append(np.stack([eng.decode_step().cpu().numpy() for _ in range(ocfg.gen_len)]))
+            meta.append((eng.counter.cpu().numpy(), eng.lastf.cpu().numpy(), eng.s_host, eng.iteration))
+        finally:
+            eng.close()
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(meta[0][0], meta[1][0])
+    np.testing.assert_array_equal(meta[0][1], meta[1][1])
+    assert meta[0][2:] == meta[1][2:]

@@ -109,11 +109,15 @@ def test_layer_pipeline_full_size(name, B, Hg, s):
         _lib.call("ig_fetch", pool.dev, idx.data_ptr(), n.data_ptr(), B, Hg, S, cap, row_bytes,
                   stage.data_ptr(), 32, 1024, hs)
         stage_tma = torch.empty_like(stage)
-        _lib.call("ig_fetch_tma", pool.dev, idx.data_ptr(), n.data_ptr(), B, Hg, S, cap, row_bytes,
-                  stage_tma.data_ptr(), 16, 1, 32, hs)
+        _lib.call("ig_fetch_tma", pool.dev, idx.data_ptr(), n.data_ptr(), None, B, Hg, S, cap,
+                  row_bytes, stage_tma.data_ptr(), 16, 1, 32, hs)
         stage_tma2 = torch.empty_like(stage)
-        _lib.call("ig_fetch_tma", pool.dev, idx.data_ptr(), n.data_ptr(), B, Hg, S, cap, row_bytes,
-                  stage_tma2.data_ptr(), 40, 2, 7, hs)
+        _lib.call("ig_fetch_tma", pool.dev, idx.data_ptr(), n.data_ptr(), None, B, Hg, S, cap,
+                  row_bytes, stage_tma2.data_ptr(), 40, 2, 7, hs)
+        full = torch.empty(B, Hg, S, 2 * d, dtype=torch.float16, device=dev)   # identity mode
+        _lib.call("ig_fetch_tma", pool.dev, None, None, st.data_ptr(), B, Hg, S, S, row_bytes,
+                  full.data_ptr(), 32, 1, 16, hs)
+        assert torch.equal(full[:, :, :s], rows_dev[:, :, :s])
         for b in range(B):
             nn = int(n_np[b])
             want = torch.gather(rows_dev[b], 1, idx[b, :, :nn].long()[..., None].expand(Hg, nn, 2 * d))
