@@ -334,12 +334,19 @@ def run_b200(a) -> None:
         f_ms = sum(stats[k]["ms"] for k in fetch_keys)
         f_launch = sum(stats[k]["launches"] for k in fetch_keys)
         fetch_gbs = f_bytes / (f_ms * 1e6) if f_ms else None
+        per_launch = f_bytes / max(f_launch, 1)
+        tr = _traffic_ratios()
         roof = {"kernel": f"fetch (ig_fetch{'_tma' if a.fetch_impl == 'tma' else ''} gather + "
                           "ig_fetch_all copy-engine rows)",
                 "bound": "host_link", "achieved": fetch_gbs, "peak": link_peak["gbs"],
                 "peak_source": link_peak["source"], "unit": "GB/s",
-                "frac": (fetch_gbs / link_peak["gbs"]) if fetch_gbs else None, "traffic": None,
-                "bytes_per_launch": f_bytes / max(f_launch, 1),
+                "frac": (fetch_gbs / link_peak["gbs"]) if fetch_gbs else None,
+                "traffic": per_launch * tr["fetch"]["sysmem_per_payload"] if tr else None,
+                "traffic_pcie": per_launch * tr["fetch"]["pcie_per_payload"] if tr else None,
+                "traffic_source": ("host-memory bytes read (and raw PCIe bytes) per algorithmic byte from "
+                                   "the committed ncu capture profiles/r01_traffic.json, scaled to this "
+                                   "run's average launch") if tr else None,
+                "bytes_per_launch": per_launch,
                 "step_share": f_ms / ms if ms else None}
         hbm = {}
         for k in ("rehearse_count", "attend", "select", "dense_ffn_in"):   # alone: own roofline
@@ -349,6 +356,8 @@ def run_b200(a) -> None:
                           "frac": gbs / hbm_peak, "bytes_per_launch": iso[k]["bytes"],
                           "ms_per_launch": iso[k]["ms"],
                           "how": f"alone on the GPU (fetch stream idle), layer {eng.L // 2}, best of 5"}
+                if k == "rehearse_count" and tr and "rehearse_count" in tr:
+                    hbm[k]["traffic"] = iso[k]["bytes"] * tr["rehearse_count"]["dram_per_algorithmic"]
         for k in ("rehearse", "attend", "select"):          # in situ, sharing the GPU with the gather
             if k in stats:
                 gbs = stats[k]["gbs"]
@@ -387,6 +396,15 @@ def run_b200(a) -> None:
     eng.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def _traffic_ratios():
+    """Per-algorithmic-byte traffic measured by ncu (committed with the repo)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
 
 
 def _graph_stats(eng, steps) -> dict:
