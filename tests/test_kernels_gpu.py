@@ -292,3 +292,64 @@ def test_attend_tma_variant_matches(monkeypatch):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(f))
     np.testing.assert_allclose(outs[0], outs[1], rtol=1e-5, atol=1e-6)
+
+
+def test_shim_error_paths_match_reference():
+    """The reference's exception behaviour at the boundary (speculation.py:51-54,
+    107-114, 124-132, 149-153; pool.py:32-33, 61-64, 91-92; model.py:167-170)."""
+    import paper_2406_19707_b200 as G
+    cfg = G.SpeculationConfig()
+    with pytest.raises(ValueError):
+        G.select_tokens([], cfg)
+    with pytest.raises(ValueError):
+        G.select_tokens([np.zeros(0, np.float32)], cfg)
+    with pytest.raises(ValueError):
+        G.select_tokens([np.zeros(4, np.float32), np.zeros(5, np.float32)], cfg)
+    with pytest.raises(ValueError):
+        G.select_tokens([np.zeros(4, np.float32)], G.SpeculationConfig(alpha=0.0))
+    with pytest.raises(ValueError):
+        G.build_partial(np.zeros((3, 4)), np.zeros((3, 5)), 0.3)
+    with pytest.raises(ValueError):
+        G.build_partial(np.zeros((3, 4)), np.zeros((3, 4)), 0.0)
+    arts = G.PartialArtifacts(3, 1)
+    arts.set_head(1, 0, G.HeadArtifacts(np.array([0, 2]), np.zeros((8, 2), np.float32),
+                                        np.zeros((0, 2), np.float32)))
+    with pytest.raises(ValueError):                     # empty partial key cache
+        G.speculate_scores(np.zeros(8, np.float32), arts, 1, 4)
+    with pytest.raises(ValueError):
+        arts.set_head(0, 0, arts.head(1, 0))            # layer 0 never speculates
+    arts.append_partial_key(1, 0, np.arange(4, dtype=np.float32), 0, 1)
+    np.testing.assert_array_equal(arts.head(1, 0).partial_k, [[0.0, 2.0]])
+    with pytest.raises(G.ArtifactConsistencyError):
+        arts.append_partial_key(1, 0, np.arange(4, dtype=np.float32), 5, 2)
+    with pytest.raises(G.ArtifactConsistencyError):
+        arts.append_partial_key(1, 0, np.arange(4, dtype=np.float32), 1, 7)
+    with pytest.raises(ValueError):
+        G.KvPool(4, limit=0)
+    p = G.KvPool(4, limit=2)
+    with pytest.raises(ValueError):
+        p.append(np.zeros(3), np.zeros(4))
+    with pytest.raises(ValueError):
+        p.evict_select()                                # empty pool
+    assert p.append(np.ones(4), np.ones(4)) == 0
+    with pytest.raises(IndexError):
+        p.fetch([1])
+    with pytest.raises(IndexError):
+        p.fetch([-1])
+    K, V = p.fetch([])                                  # empty fetch is legal
+    assert K.shape == (0, 4)
+    p.close()
+    with pytest.raises(ValueError):
+        G.attention_head(np.zeros((1, 4)), np.zeros((2, 4)), np.zeros((3, 4)))
+
+
+def test_select_all_rows_and_single_row():
+    """n == s (alpha huge, cap 1.0) selects every row; s == 1 selects row 0."""
+    import paper_2406_19707_b200 as G
+    sc = [np.random.default_rng(0).standard_normal(37).astype(np.float32) for _ in range(3)]
+    picks, n = G.select_tokens(sc, G.SpeculationConfig(0.3, 1e9, 1.0, 1))
+    assert n == 37
+    for h in range(3):
+        np.testing.assert_array_equal(picks[h], O.topk_indices(sc[h], 37))
+    picks, n = G.select_tokens([np.array([2.5], np.float32)], G.SpeculationConfig())
+    assert n == 1 and list(picks[0]) == [0]
