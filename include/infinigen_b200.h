@@ -178,6 +178,38 @@ int ig_attend(const float* q, int ldq, const float* k_cur, const float* v_cur, i
               const int32_t* pos, const ig_step_state* st, int B, int Hg, int d, int cap,
               float* partial, int32_t* tickets, float* out, int ldo, void* stream);
 
+/* ---- resident selection (B200 extension of K3/K4) ----------
+ * The fetched set of each speculative layer stays in HBM across decode steps
+ * in a slot table: stage T[B][Hg][cap][2][d], slot_id i32[B][Hg][cap] (row
+ * index held by the slot, -1 = empty), slot_used i32[B][Hg] (slots in use).
+ * Only rows that enter the selection are fetched from the host pool, which
+ * stays authoritative (the reference refetches every selected row each step,
+ * pool.py:83-99 via engine.py:352-356; same rows, fewer link bytes).
+ *
+ * ig_resident_plan, per (b, h): free every slot whose row is not in the new
+ * ascending selection idx[b,h,0:n[b]] or equals pos_prev[b,h] (the row last
+ * step's append overwrote; NULL = none), then give the selected rows that are
+ * not resident the free slots in ascending order (then slots from slot_used
+ * up): fetch list frow/fslot i32[B][Hg][cap], fcount i32[B][Hg].  moved_rows
+ * (nullable) accumulates the fetched row count.  Shared memory 5*cap bytes.
+ * ig_fetch_slots: stage[b,h,fslot[k]] = pool[b,h,frow[k]] for k < fcount.
+ * ig_stage_put: stage[b,h,pos[b,h]] = (k_cur, v_cur) rounded to `elt` exactly
+ * like ig_append (layer 0's full mirror, stage rows per (b, h) = stage_rows).
+ * ig_attend_slots: ig_attend over slots r < slot_used[b,h] whose id >= 0 and
+ * != pos, plus the current row.                                            */
+int ig_resident_plan(const int32_t* idx, const int32_t* n, const int32_t* pos_prev,
+                     int32_t* slot_id, int32_t* slot_used, int B, int Hg, int cap, int32_t* frow,
+                     int32_t* fslot, int32_t* fcount, uint64_t* moved_rows, void* stream);
+int ig_fetch_slots(const void* pool_dev, const int32_t* frow, const int32_t* fslot,
+                   const int32_t* fcount, int B, int Hg, int S_max, int cap, int row_bytes,
+                   void* stage, void* stream);
+int ig_stage_put(const float* k_cur, const float* v_cur, int ldkv, const int32_t* pos, void* stage,
+                 int elt, int B, int Hg, int d, int stage_rows, void* stream);
+int ig_attend_slots(const float* q, int ldq, const float* k_cur, const float* v_cur, int ldkv,
+                    const void* stage, int elt, const int32_t* slot_id, const int32_t* slot_used,
+                    const int32_t* pos, const ig_step_state* st, int B, int Hg, int d, int cap,
+                    float* partial, int32_t* tickets, float* out, int ldo, void* stream);
+
 /* Strided 2-D copy between any UVA addresses (cudaMemcpyDefault): used to
  * write prefill K/V rows into the host pool (engine.py:265-266).          */
 int ig_memcpy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,

@@ -47,6 +47,11 @@ _SIGS = {
     "ig_score_max": [_P, _P, _I, _I, _I, _P, _P],
     "ig_attend_scratch": [_I, _I, _I, _I, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ)],
     "ig_attend": [_P, _I, _P, _P, _I, _P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _I, _P],
+    "ig_attend_slots": [_P, _I, _P, _P, _I, _P, _I, _P, _P, _P, _P, _I, _I, _I, _I, _P, _P, _P, _I,
+                        _P],
+    "ig_resident_plan": [_P, _P, _P, _P, _P, _I, _I, _I, _P, _P, _P, _P, _P],
+    "ig_fetch_slots": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P],
+    "ig_stage_put": [_P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _P],
     "ig_memcpy2d": [_P, _SZ, _P, _SZ, _SZ, _SZ, _P],
     "ig_sgemm_rows_ksplit": [_I, _I, _I],
     "ig_sgemm_rows": [_P, _I, _P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _I, _P, _SZ, _P, _P],

@@ -19,6 +19,13 @@ constexpr int kAttChunk = 128;     // staged rows per CTA
 constexpr int kAttMaxPer = 8;      // head_dim <= 256
 constexpr int kAttRowsInFlight = 4;
 
+// Rows of one (b, h): a per-head count (resident slot tables), the step's
+// shared n (selection), or every pool row (identity, layer 0).
+__device__ __forceinline__ int att_rows(const int32_t* rows_bh, const int32_t* n_in,
+                                        const ig_step_state* st, int b, size_t bh) {
+  return rows_bh ? rows_bh[bh] : (n_in ? n_in[b] : st->s_len);
+}
+
 // Lane l owns elements l*E .. l*E+E-1 when E > 0 (d == 32*E, vector loads);
 // for other head dims (E == 0) lane l owns l, l+32, ... (scalar loads).
 template <typename T, int E>
@@ -39,7 +46,7 @@ __global__ void __launch_bounds__(kAttThreads)
 attend_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_cur,
               const float* __restrict__ v_cur, int ldkv, const T* __restrict__ stage,
               const int32_t* __restrict__ idx, const int32_t* __restrict__ n_in,
-              const int32_t* __restrict__ pos_in, const ig_step_state* __restrict__ st, int Hg,
+              const int32_t* __restrict__ rows_bh, const int32_t* __restrict__ pos_in, const ig_step_state* __restrict__ st, int Hg,
               int d, int cap, float inv_dummy, float sqrt_d, int max_chunks,
               float* __restrict__ partial, int32_t* __restrict__ tickets, float* __restrict__ out,
               int ldo) {
@@ -47,7 +54,7 @@ attend_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_
   constexpr int P = IO::kPer;
   const int b = blockIdx.z, h = blockIdx.y, c = blockIdx.x;
   const size_t bh = (size_t)b * Hg + h;
-  const int rows = n_in ? n_in[b] : st->s_len;
+  const int rows = att_rows(rows_bh, n_in, st, b, bh);
   const int nchunks = max(1, (rows + kAttChunk - 1) / kAttChunk);
   if (c >= nchunks) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -84,7 +91,8 @@ attend_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_
 #pragma unroll
     for (int u = 0; u < kAttRowsInFlight; ++u) {
       const int r = rb + u;
-      ok[u] = r < r1 && (idx ? idx[bh * cap + r] : r) != pos;
+      const int id = r < r1 ? (idx ? idx[bh * cap + r] : r) : -1;
+      ok[u] = id >= 0 && id != pos;   // id < 0: empty resident slot
       if (ok[u]) {
         IO::load(base + (size_t)r * 2 * d, lane, d, kk[u]);
         IO::load(base + (size_t)r * 2 * d + d, lane, d, vv[u]);
@@ -193,13 +201,13 @@ __global__ void __launch_bounds__(kAttThreads)
 attend512_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_cur,
                  const float* __restrict__ v_cur, int ldkv, const T* __restrict__ stage,
                  const int32_t* __restrict__ idx, const int32_t* __restrict__ n_in,
-                 const int32_t* __restrict__ pos_in, const ig_step_state* __restrict__ st, int Hg,
+                 const int32_t* __restrict__ rows_bh, const int32_t* __restrict__ pos_in, const ig_step_state* __restrict__ st, int Hg,
                  int cap, float sqrt_d, int max_chunks, float* __restrict__ partial,
                  int32_t* __restrict__ tickets, float* __restrict__ out, int ldo) {
   constexpr int d = 128;
   const int b = blockIdx.z, h = blockIdx.y, c = blockIdx.x;
   const size_t bh = (size_t)b * Hg + h;
-  const int rows = n_in ? n_in[b] : st->s_len;
+  const int rows = att_rows(rows_bh, n_in, st, b, bh);
   const int nchunks = max(1, (rows + kFastChunk - 1) / kFastChunk);
   if (c >= nchunks) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -276,8 +284,9 @@ attend512_kernel(const float* __restrict__ q, int ldq, const float* __restrict__
 #pragma unroll
     for (int u = 0; u < kFastRows; ++u) {
       const int id = idx ? __shfl_sync(0xffffffffu, rowid, u) : rb + u;
-      const bool ok = rb + u < r1 && id != pos;
+      const bool ok = rb + u < r1 && id >= 0 && id != pos;   // id < 0: empty slot
       dot[u] = ok ? __shfl_sync(0xffffffffu, dot[u], 0) / sqrt_d : -INFINITY;
+      if (!ok) raw[u] = make_uint4(0u, 0u, 0u, 0u);   // p = 0 must not meet stale bits
       gm = fmaxf(gm, dot[u]);
     }
     if (gm != -INFINITY) {        // warp-uniform
@@ -396,7 +405,7 @@ __global__ void __launch_bounds__(kAttThreads)
 attend512_tma_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_cur,
                      const float* __restrict__ v_cur, int ldkv, const T* __restrict__ stage,
                      const int32_t* __restrict__ idx, const int32_t* __restrict__ n_in,
-                     const int32_t* __restrict__ pos_in, const ig_step_state* __restrict__ st,
+                     const int32_t* __restrict__ rows_bh, const int32_t* __restrict__ pos_in, const ig_step_state* __restrict__ st,
                      int Hg, int cap, float sqrt_d, int max_chunks, float* __restrict__ partial,
                      int32_t* __restrict__ tickets, float* __restrict__ out, int ldo) {
   constexpr int d = 128;
@@ -404,7 +413,7 @@ attend512_tma_kernel(const float* __restrict__ q, int ldq, const float* __restri
   __shared__ __align__(8) unsigned long long bars[kTmaStages];
   const int b = blockIdx.z, h = blockIdx.y, c = blockIdx.x;
   const size_t bh = (size_t)b * Hg + h;
-  const int rows = n_in ? n_in[b] : st->s_len;
+  const int rows = att_rows(rows_bh, n_in, st, b, bh);
   const int nchunks = max(1, (rows + kTmaChunk - 1) / kTmaChunk);
   if (c >= nchunks) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -466,8 +475,9 @@ attend512_tma_kernel(const float* __restrict__ q, int ldq, const float* __restri
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int id = idx ? __shfl_sync(0xffffffffu, rowid, u) : rb + u;
-      const bool ok = rb + u < r1 && id != pos;
+      const bool ok = rb + u < r1 && id >= 0 && id != pos;   // id < 0: empty slot
       dot[u] = ok ? __shfl_sync(0xffffffffu, dot[u], 0) / sqrt_d : -INFINITY;
+      if (!ok) raw[u] = make_uint4(0u, 0u, 0u, 0u);   // p = 0 must not meet stale bits
       gm = fmaxf(gm, dot[u]);
     }
     if (gm != -INFINITY) {
@@ -576,9 +586,9 @@ inline bool attend_tma_enabled() {
 template <typename T>
 int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const float* k_cur,
                   const float* v_cur, int ldkv, const void* stage, const int32_t* idx,
-                  const int32_t* n, const int32_t* pos, const ig_step_state* st, int Hg, int d,
-                  int cap, float sqrt_d, int max_chunks, float* partial, int32_t* tickets,
-                  float* out, int ldo) {
+                  const int32_t* n, const int32_t* rows_bh, const int32_t* pos,
+                  const ig_step_state* st, int Hg, int d, int cap, float sqrt_d, int max_chunks,
+                  float* partial, int32_t* tickets, float* out, int ldo) {
   if constexpr (sizeof(T) == 2) {
     if (d == 128 && attend_tma_enabled()) {  // 512-B rows, TMA-fed (opt-in)
       const int mc = (cap + kTmaChunk - 1) / kTmaChunk;
@@ -586,7 +596,7 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
       IG_CUDA_STATUS(cudaFuncSetAttribute(attend512_tma_kernel<T>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       attend512_tma_kernel<T><<<dim3(mc, grid.y, grid.z), kAttThreads, smem, s>>>(
-          q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, pos, st, Hg, cap, sqrt_d,
+          q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, Hg, cap, sqrt_d,
           max_chunks, partial, tickets, out, ldo);
       IG_LAUNCH_STATUS();
       return IG_OK;
@@ -594,7 +604,7 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
     if (d == 128) {  // 512-B rows, register-fed (default)
       const int mc = (cap + kFastChunk - 1) / kFastChunk;
       attend512_kernel<T><<<dim3(mc, grid.y, grid.z), kAttThreads, 0, s>>>(
-          q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, pos, st, Hg, cap, sqrt_d,
+          q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, Hg, cap, sqrt_d,
           max_chunks, partial, tickets, out, ldo);
       IG_LAUNCH_STATUS();
       return IG_OK;
@@ -602,8 +612,8 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
   }
 #define IG_ATT(E)                                                                              \
   attend_kernel<T, E><<<grid, kAttThreads, 0, s>>>(q, ldq, k_cur, v_cur, ldkv,                \
-      (const T*)stage, idx, n, pos, st, Hg, d, cap, 0.f, sqrt_d, max_chunks, partial, tickets, \
-      out, ldo)
+      (const T*)stage, idx, n, rows_bh, pos, st, Hg, d, cap, 0.f, sqrt_d, max_chunks, partial, \
+      tickets, out, ldo)
   switch (d) {
     case 32: IG_ATT(1); break;
     case 64: IG_ATT(2); break;
@@ -628,11 +638,12 @@ extern "C" int ig_attend_scratch(int B, int Hg, int d, int cap, size_t* partial_
   return IG_OK;
 }
 
-extern "C" int ig_attend(const float* q, int ldq, const float* k_cur, const float* v_cur, int ldkv,
-                         const void* stage, int elt, const int32_t* idx, const int32_t* n,
-                         const int32_t* pos, const ig_step_state* st, int B, int Hg, int d, int cap,
-                         float* partial, int32_t* tickets, float* out, int ldo, void* stream) {
-  using namespace ig;
+namespace ig {
+static int attend_dispatch(const float* q, int ldq, const float* k_cur, const float* v_cur,
+                           int ldkv, const void* stage, int elt, const int32_t* idx,
+                           const int32_t* n, const int32_t* rows_bh, const int32_t* pos,
+                           const ig_step_state* st, int B, int Hg, int d, int cap, float* partial,
+                           int32_t* tickets, float* out, int ldo, void* stream) {
   if (!q || !k_cur || !v_cur || !stage || !pos || !st || !partial || !tickets || !out || B < 1 ||
       Hg < 1 || d < 1 || d > 32 * kAttMaxPer || cap < 1 || ldq < Hg * d || ldkv < Hg * d ||
       ldo < Hg * d)
@@ -643,16 +654,37 @@ extern "C" int ig_attend(const float* q, int ldq, const float* k_cur, const floa
   cudaStream_t s = (cudaStream_t)stream;
   switch (elt) {
     case IG_ELT_F32:
-      return launch_attend<float>(grid, s, q, ldq, k_cur, v_cur, ldkv, stage, idx, n, pos, st, Hg,
-                                  d, cap, sqrt_d, max_chunks, partial, tickets, out, ldo);
+      return launch_attend<float>(grid, s, q, ldq, k_cur, v_cur, ldkv, stage, idx, n, rows_bh, pos,
+                                  st, Hg, d, cap, sqrt_d, max_chunks, partial, tickets, out, ldo);
     case IG_ELT_F16:
-      return launch_attend<__half>(grid, s, q, ldq, k_cur, v_cur, ldkv, stage, idx, n, pos, st,
-                                   Hg, d, cap, sqrt_d, max_chunks, partial, tickets, out, ldo);
+      return launch_attend<__half>(grid, s, q, ldq, k_cur, v_cur, ldkv, stage, idx, n, rows_bh,
+                                   pos, st, Hg, d, cap, sqrt_d, max_chunks, partial, tickets, out,
+                                   ldo);
     case IG_ELT_BF16:
-      return launch_attend<__nv_bfloat16>(grid, s, q, ldq, k_cur, v_cur, ldkv, stage, idx, n, pos,
-                                          st, Hg, d, cap, sqrt_d, max_chunks, partial, tickets,
-                                          out, ldo);
+      return launch_attend<__nv_bfloat16>(grid, s, q, ldq, k_cur, v_cur, ldkv, stage, idx, n,
+                                          rows_bh, pos, st, Hg, d, cap, sqrt_d, max_chunks,
+                                          partial, tickets, out, ldo);
     default:
       return IG_EINVAL;
   }
+}
+}  // namespace ig
+
+extern "C" int ig_attend(const float* q, int ldq, const float* k_cur, const float* v_cur, int ldkv,
+                         const void* stage, int elt, const int32_t* idx, const int32_t* n,
+                         const int32_t* pos, const ig_step_state* st, int B, int Hg, int d, int cap,
+                         float* partial, int32_t* tickets, float* out, int ldo, void* stream) {
+  return ig::attend_dispatch(q, ldq, k_cur, v_cur, ldkv, stage, elt, idx, n, nullptr, pos, st, B,
+                             Hg, d, cap, partial, tickets, out, ldo, stream);
+}
+
+extern "C" int ig_attend_slots(const float* q, int ldq, const float* k_cur, const float* v_cur,
+                               int ldkv, const void* stage, int elt, const int32_t* slot_id,
+                               const int32_t* slot_used, const int32_t* pos,
+                               const ig_step_state* st, int B, int Hg, int d, int cap,
+                               float* partial, int32_t* tickets, float* out, int ldo,
+                               void* stream) {
+  if (!slot_id || !slot_used) return IG_EINVAL;
+  return ig::attend_dispatch(q, ldq, k_cur, v_cur, ldkv, stage, elt, slot_id, nullptr, slot_used,
+                             pos, st, B, Hg, d, cap, partial, tickets, out, ldo, stream);
 }

@@ -159,13 +159,20 @@ class DecodeEngine:
         keep layer 0's rows -- which every step reads in full (engine.py:393-396)
         -- resident in HBM, so they never cross the host link.  Traces keep the
         reference byte accounting; bench.py reports moved bytes separately.
+    resident : keep each speculative layer's fetched set in HBM across steps
+        (a slot table of at most `cap` rows per (layer, seq, head)) and fetch
+        only the rows that enter the selection; layer 0's rows are mirrored in
+        HBM and the appended row is written to the mirror in the same step.
+        The host pool stays authoritative (every append still goes to it) and
+        the attended rows, selections and traces are those of the default path
+        (csrc/resident.cu).
     """
 
     def __init__(self, model, config: RunConfig, *, max_steps: int | None = None,
                  pool_dtype: str = "f16", device=None, group=None, fetch_ctas: int = 32,
                  fetch_threads: int = 32, fetch_priority: int = 0, hbm_layers: int = 0,
                  fetch_impl: str = "tma", fetch_rows: int = 16, dense: str = "ig",
-                 cuda_graph: bool = False):
+                 cuda_graph: bool = False, resident: bool = False):
         config.validate()
         _lib.load()
         _enable_ieee_fp32()
@@ -219,6 +226,10 @@ class DecodeEngine:
         if hbm_layers not in (0, 1) or hbm_layers > spec.layers:
             raise ValueError("hbm_layers must be 0 or 1")
         self.hbm_layers = hbm_layers
+        if resident and (scheme != "speculative" or hbm_layers):
+            raise ValueError("resident needs the speculative scheme and hbm_layers=0")
+        self.resident = bool(resident)
+        self._res_valid = False
         self.scale = float(np.float32(1.0 / np.sqrt(d)))   # speculation.py:127
         self._load_weights(model)
         self._alloc()
@@ -228,6 +239,7 @@ class DecodeEngine:
         self.records: list = []       # per iteration: [B][L] record dicts
         self.prefill_info: dict = {}
         self._prefetched0 = False
+        self._res_valid = False
 
     # ------------------------------------------------------------------ setup
     def _load_weights(self, model) -> None:
@@ -281,7 +293,17 @@ class DecodeEngine:
         self.stage_full = [torch.empty((B, Hg, S, 2 * d), dtype=T, device=dev)
                            for _ in range(1 if spec_ else 2)]
         self.stage_sel = [torch.empty((B, Hg, cap, 2 * d), dtype=T, device=dev)
-                          for _ in range(2 if spec_ else 0)]
+                          for _ in range(2 if spec_ and not self.resident else 0)]
+        if self.resident:
+            Lr = max(L - 1, 1)
+            # zero-filled: a slot never written must not hold NaN bits
+            self.stage_res = torch.zeros((Lr, B, Hg, cap, 2 * d), dtype=T, device=dev)
+            self.slot_id = torch.full((Lr, B, Hg, cap), -1, dtype=i32, device=dev)
+            self.slot_used = torch.zeros((Lr, B, Hg), dtype=i32, device=dev)
+            self.frow = torch.zeros((2, B, Hg, cap), dtype=i32, device=dev)
+            self.fslot = torch.zeros((2, B, Hg, cap), dtype=i32, device=dev)
+            self.fcount = torch.zeros((2, B, Hg), dtype=i32, device=dev)
+            self.moved_rows = torch.zeros(L, dtype=i64, device=dev)
         # skinny-GEMM workspace: the largest ceil(N/128) * ksplit * B * 128 over the projections
         shapes = [(3 * Hg * d, D), (Hg * d, D), (D, Hg * d), (F, D), (D, F)]   # (N, K)
         ws = 0
@@ -346,6 +368,7 @@ class DecodeEngine:
             self.pool_hbm = None
         self.hbm_layers = n
         self._prefetched0 = False
+        self._res_valid = False
         self._graph = None
 
     def _pool_layer_dev(self, li: int) -> int:
@@ -416,6 +439,7 @@ class DecodeEngine:
         self.x.copy_(_f32(x, self.device).reshape(self.B, self.D))
         self._set_state(s_len, seq0)
         self._prefetched0 = False
+        self._res_valid = False
         self._graph = None
         torch.cuda.synchronize(self.device)
 
@@ -495,6 +519,7 @@ class DecodeEngine:
         self.counter[..., :rows] = torch.from_numpy(ct).to(self.device)
         self._set_state(rows, N)
         self._prefetched0 = False
+        self._res_valid = False
         self._graph = None
         self.prefill_info = {"prompt_len": N, "pool_rows": rows,
                              "partial_cols": self.kcols if (self.scheme == "speculative" and L > 1) else None,
@@ -509,6 +534,9 @@ class DecodeEngine:
         are asynchronous: no host synchronisation is added."""
         self._inst = {"steps": steps, "k": 0, "ev": [], "s": [],
                       "n": torch.zeros((steps, self.L, self.B), dtype=torch.int32, device=self.device)}
+        if self.resident:   # rows actually fetched per (step, layer): moved_rows snapshots
+            self._inst["moved0"] = self.moved_rows.clone()
+            self._inst["moved"] = torch.zeros((steps, self.L), dtype=torch.int64, device=self.device)
 
     def _mark(self, kind: str, li: int, stream, start: bool):
         inst = self._inst
@@ -531,12 +559,18 @@ class DecodeEngine:
         torch.cuda.synchronize(self.device)
         n_hist = inst["n"].cpu().numpy()
         B, Hg, d, kc, rb = self.B, self.Hg, self.d, self.kcols, self.row_bytes
+        moved = None
+        if "moved" in inst:
+            snap = np.concatenate([inst["moved0"].cpu().numpy()[None], inst["moved"].cpu().numpy()])
+            moved = np.diff(snap, axis=0)                 # [step][layer] rows fetched
         out = {}
         for k, kind, li, e0, e1 in inst["ev"]:
             if e1 is None:
                 continue
             s = inst["s"][k]
-            if kind == "fetch":
+            if kind == "fetch" and moved is not None and li >= 1:
+                nbytes = int(moved[k, li]) * rb           # resident: rows that entered the set
+            elif kind == "fetch":
                 rows = B * s if (li == 0 or self.scheme == "full") else int(n_hist[k, li].sum())
                 nbytes = rows * Hg * rb
             elif kind == "rehearse":
@@ -546,7 +580,9 @@ class DecodeEngine:
             else:                                             # attend: staged rows read
                 rows = B * s if (li == 0 or self.scheme == "full") else int(n_hist[k, li].sum())
                 nbytes = rows * Hg * rb
-            tag = kind if kind != "fetch" else ("fetch_all_ce" if (li == 0 or self.scheme == "full") else "fetch_gather")
+            tag = kind if kind != "fetch" else (
+                "fetch_all_ce" if (li == 0 or self.scheme == "full")
+                else ("fetch_slots" if moved is not None else "fetch_gather"))
             r = out.setdefault(tag, {"launches": 0, "ms": 0.0, "bytes": 0})
             r["launches"] += 1
             r["ms"] += e0.elapsed_time(e1)
@@ -602,7 +638,10 @@ class DecodeEngine:
                       int(sc.min_select), idx_tmp.data_ptr(), n_tmp.data_ptr(), self.err.data_ptr(), h)
 
         def attend():
-            self._attend(li, self.stage_sel[li % 2], self.idx[li], self.n[li], self.cap, h)
+            if self.resident:
+                self._attend_slots(li, h)
+            else:
+                self._attend(li, self.stage_sel[li % 2], self.idx[li], self.n[li], self.cap, h)
 
         hid = torch.empty_like(self.hidden)
 
@@ -662,6 +701,16 @@ class DecodeEngine:
                   self.B, self.Hg, self.d, stage_rows, self.att_partial.data_ptr(),
                   self.att_tickets.data_ptr(), self.attn.data_ptr(), Hgd, cs)
 
+    def _attend_slots(self, li: int, cs: int) -> None:
+        Hgd = self.Hg * self.d
+        q = self.qkv
+        _lib.call("ig_attend_slots", q.data_ptr(), 3 * Hgd, q.data_ptr() + 4 * Hgd,
+                  q.data_ptr() + 8 * Hgd, 3 * Hgd, self.stage_res[li - 1].data_ptr(),
+                  _lib.ELT[self.elt], self.slot_id[li - 1].data_ptr(),
+                  self.slot_used[li - 1].data_ptr(), self.pos[li].data_ptr(), self.st.data_ptr(),
+                  self.B, self.Hg, self.d, self.cap, self.att_partial.data_ptr(),
+                  self.att_tickets.data_ptr(), self.attn.data_ptr(), Hgd, cs)
+
     @torch.no_grad()
     def decode_step(self) -> torch.Tensor:
         """One decode iteration for all B sequences; returns x [B, D] on the
@@ -718,7 +767,19 @@ class DecodeEngine:
         with torch.cuda.stream(C):
             self.count_sum.zero_()
             self.ev_step.record(C)
-            if self.hbm_layers:
+            resident = self.resident
+            if resident and self._res_valid:
+                self.ev_fetch[0].record(C)          # layer 0 mirrored in HBM: no fetch
+            elif resident:                          # (re)start: empty slot tables, full layer 0
+                self.slot_id.fill_(-1)
+                self.slot_used.zero_()
+                Fs.wait_event(self.ev_step)
+                if graph:
+                    self._issue_full_fetch_dev(0, self.stage_full[0])
+                else:
+                    self._issue_full_fetch(0, s, self.stage_full[0])
+                self.ev_fetch[0].record(Fs)
+            elif self.hbm_layers:
                 self.ev_fetch[0].record(C)          # layer 0 is HBM-resident: no fetch
             elif graph:                             # in-step, row count read on the device
                 Fs.wait_event(self.ev_step)
@@ -756,10 +817,25 @@ class DecodeEngine:
                         self._mark("select", nxt, C, False)
                         if cfg.record_scores:
                             spec_scores[nxt] = self.scores[:, :, :s].cpu()
+                        if resident:
+                            par = nxt % 2
+                            _lib.call("ig_resident_plan", self.idx[nxt].data_ptr(),
+                                      self.n[nxt].data_ptr(), self.pos[nxt].data_ptr(),
+                                      self.slot_id[nxt - 1].data_ptr(),
+                                      self.slot_used[nxt - 1].data_ptr(), B, Hg, self.cap,
+                                      self.frow[par].data_ptr(), self.fslot[par].data_ptr(),
+                                      self.fcount[par].data_ptr(),
+                                      self.moved_rows[nxt].data_ptr(), cs)
                         self.ev_sel[nxt].record(C)
                         Fs.wait_event(self.ev_sel[nxt])
                         self._mark("fetch", nxt, Fs, True)
-                        if self.fetch_impl == "tma":
+                        if resident:
+                            _lib.call("ig_fetch_slots", self._pool_layer_dev(nxt),
+                                      self.frow[par].data_ptr(), self.fslot[par].data_ptr(),
+                                      self.fcount[par].data_ptr(), B, Hg, self.S_max, self.cap,
+                                      self.row_bytes, self.stage_res[nxt - 1].data_ptr(),
+                                      Fs.cuda_stream)
+                        elif self.fetch_impl == "tma":
                             _lib.call("ig_fetch_tma", self._pool_layer_dev(nxt),
                                       self.idx[nxt].data_ptr(), self.n[nxt].data_ptr(), None, B,
                                       Hg, self.S_max, self.cap, self.row_bytes,
@@ -794,9 +870,16 @@ class DecodeEngine:
                           _lib.ptr(self.n[li]) if sel else None, self.cap,
                           self.st.data_ptr(), B, Hg, d, self.S_max, self.pos[li].data_ptr(),
                           self.events[li].data_ptr(), cs)
+                if resident and li == 0:            # keep layer 0's mirror complete
+                    _lib.call("ig_stage_put", self.qkv.data_ptr() + 4 * Hgd,
+                              self.qkv.data_ptr() + 8 * Hgd, 3 * Hgd, self.pos[0].data_ptr(),
+                              self.stage_full[0].data_ptr(), _lib.ELT[self.elt], B, Hg, d,
+                              self.S_max, cs)
                 C.wait_event(self.ev_fetch[li])
                 self._mark("attend", li, C, True)
-                if sel:
+                if sel and resident:
+                    self._attend_slots(li, cs)
+                elif sel:
                     self._attend(li, self.stage_sel[li % 2], self.idx[li], self.n[li], self.cap, cs)
                 elif li < self.hbm_layers:
                     self._attend(li, self.pool_hbm[li], None, None, self.S_max, cs)
@@ -823,6 +906,8 @@ class DecodeEngine:
             inst = self._inst
             if inst is not None and not graph and inst["k"] < inst["steps"]:
                 inst["n"][inst["k"]].copy_(self.n)
+                if "moved" in inst:
+                    inst["moved"][inst["k"]].copy_(self.moved_rows)
                 inst["s"].append(s)
                 inst["k"] += 1
             s_next = min(s + 1, cfg.pool_limit) if cfg.pool_limit else s + 1
@@ -832,13 +917,15 @@ class DecodeEngine:
                 if x is not self.xbuf[0]:           # replays must start from xbuf[0]
                     self.xbuf[0].copy_(x)
                     x = self.xbuf[0]
-            elif not self.hbm_layers:
+            elif not self.hbm_layers and not resident:
                 last0 = 0 if speculative else (L - 1 if (L - 1) % 2 == 0 else L - 2)
                 Fs.wait_event(self.ev_att[last0])
                 self._issue_full_fetch(0, s_next, self.stage_full[0])
                 self.ev_fetch[0].record(Fs)
                 self._prefetched0 = True
             self.x = x
+        if resident:
+            self._res_valid = True
         torch.cuda.current_stream(self.device).wait_stream(C)
         self.s_host = s_next
         if speculative and L > 1 and int(self.err.item() if recording else 0):
