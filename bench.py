@@ -58,14 +58,15 @@ def _args():
     ap.add_argument("--fetch-priority", type=int, default=0, help="CUDA stream priority (-1 = high)")
     ap.add_argument("--fetch-impl", default="tma", choices=["ldg", "tma"])
     ap.add_argument("--fetch-rows", type=int, default=16, help="TMA rows per warp batch")
-    ap.add_argument("--dense", default="ig", choices=["ig", "cublas"])
+    ap.add_argument("--dense", default="tc", choices=["ig", "tc", "cublas"])
     ap.add_argument("--cuda-graph", action="store_true", help="replay a captured decode step")
-    ap.add_argument("--resident", action="store_true",
-                    help="keep each layer's fetched set in HBM across steps; fetch only new rows")
+    ap.add_argument("--no-resident", dest="resident", action="store_false",
+                    help="refetch every selected row each step (the reference's data movement) "
+                         "instead of keeping each layer's fetched set resident in HBM")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets N ranks share one GPU (tests of the N > 1 path)")
-    ap.add_argument("--no-hbm-variant", action="store_true",
-                    help="skip the secondary run with layer 0's KV resident in HBM")
+    ap.add_argument("--no-variant", "--no-hbm-variant", dest="no_variant", action="store_true",
+                    help="skip the secondary run (resident: refetch every step; else layer 0 in HBM)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-steps", type=int, default=2)
     return ap.parse_args()
@@ -205,7 +206,8 @@ def _config(a) -> dict:
             "fetch": (f"{a.fetch_impl} x {a.fetch_ctas} CTAs x {a.fetch_threads} threads"
                       + (f" x {a.fetch_rows} rows/batch" if a.fetch_impl == "tma" else "")),
             "parallelism": f"tp{a.gpus} (heads)" if a.gpus > 1 else "single GPU",
-            "dense": "ig_sgemm_rows (f32)" if a.dense == "ig" else "cuBLAS f32 (TF32 off)",
+            "dense": {"ig": "ig_sgemm_rows (f32 CUDA cores)", "tc": "ig_sgemm_tc (3xTF32 tensor cores)",
+                      "cublas": "cuBLAS f32 (TF32 off)"}[a.dense],
             "cuda_graph": bool(a.cuda_graph), "resident": bool(a.resident),
             "l2": "inputs larger than L2 (partial K >= 1.6 GB streamed per layer set; host pool 54 GB)"}
 
@@ -241,7 +243,7 @@ def run_b200(a) -> None:
     model = generate_synthetic_gpu(spec, device=dev)
     skew_model_gpu(model)
     # warmup + timed + e2e + (HBM variant: 2 + timed) decode steps, plus slack
-    steps_total = a.warmup + 3 * a.steps + 8
+    steps_total = a.warmup + 4 * a.steps + 8
     cfg = RunConfig(scheme="speculative", prompt_len=a.prompt, gen_len=steps_total, batch=a.batch,
                     speculation=SpeculationConfig(WORKLOAD["ratio"], WORKLOAD["alpha"], WORKLOAD["cap"], 1))
     eng = DecodeEngine(model, cfg, pool_dtype="f16", device=dev, group=group, fetch_ctas=a.fetch_ctas,
@@ -268,9 +270,8 @@ def run_b200(a) -> None:
         eng.decode_step()
     barrier()
     # -------- device-timed region: K steps, inputs resident in HBM / host pool
+    # (no per-kernel events here: they are recorded in a separate pass below)
     launches0 = _lib.launches
-    if not a.cuda_graph:
-        eng.instrument(a.steps)
     cur = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     prof = os.environ.get("IG_PROFILE_WINDOW") == "1"   # ncu --profile-from-start off
@@ -289,8 +290,19 @@ def run_b200(a) -> None:
     launches = _lib.launches - launches0
     if a.cuda_graph:   # one eager step's launches are replayed per step
         launches = eng.graph_launches * a.steps
-    stats = eng.kernel_stats() if not a.cuda_graph else _graph_stats(eng, a.steps)
-    eng._inst = None
+        stats = _graph_stats(eng, a.steps)
+    else:
+        # -------- per-kernel CUDA events over another K steps (not the headline)
+        eng.instrument(a.steps)
+        i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        i0.record(cur)
+        for _ in range(a.steps):
+            eng.decode_step()
+        i1.record(cur)
+        barrier()
+        stats = eng.kernel_stats()
+        stats["instrumented_ms_per_step"] = i0.elapsed_time(i1) / a.steps
+        eng._inst = None
     iso = eng.isolated_kernel_times(li=eng.L // 2) if eng.L > 2 else {}
     # -------- end-to-end: public API with host input/output rows each step
     x_host = torch.empty((a.batch, spec.model_dim), dtype=torch.float32).pin_memory()
@@ -302,10 +314,29 @@ def run_b200(a) -> None:
         x_host.copy_(torch.from_numpy(out))
     barrier()
     e2e_ms = (time.perf_counter() - t0) * 1000.0
-    # -------- secondary variant: layer 0 (read in full every step) kept in HBM
+    # -------- secondary variant: resident -> refetch every selected row each
+    # step (the reference's data movement, host-link bound); else layer 0 in HBM
     var_ms = 0.0
     var_stats = None
-    if not a.no_hbm_variant and not a.resident:
+    var_kind = None
+    if not a.no_variant and a.resident and not a.cuda_graph:
+        var_kind = "refetch"
+        eng.set_resident(False)
+        for _ in range(2):
+            eng.decode_step()
+        eng.instrument(a.steps)
+        barrier()
+        v0, v1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        v0.record(cur)
+        for _ in range(a.steps):
+            eng.decode_step()
+        v1.record(cur)
+        barrier()
+        var_ms = v0.elapsed_time(v1)
+        var_stats = eng.kernel_stats()
+        eng._inst = None
+    elif not a.no_variant and not a.resident:
+        var_kind = "layer0_in_hbm"
         eng.set_hbm_layers(1)
         for _ in range(2):
             eng.decode_step()
@@ -331,25 +362,33 @@ def run_b200(a) -> None:
         value = tok / (ms / 1000.0)
         hbm_peak = _peak("hbm_gbs", 6452.8)
         link_peak = _link_peak(dev)
-        fetch_keys = [k for k in ("fetch_gather", "fetch_slots", "fetch_all_ce") if k in stats]
-        f_bytes = sum(stats[k]["bytes"] for k in fetch_keys)
-        f_ms = sum(stats[k]["ms"] for k in fetch_keys)
-        f_launch = sum(stats[k]["launches"] for k in fetch_keys)
-        fetch_gbs = f_bytes / (f_ms * 1e6) if f_ms else None
-        per_launch = f_bytes / max(f_launch, 1)
         tr = _traffic_ratios()
-        roof = {"kernel": f"fetch (ig_fetch{'_tma' if a.fetch_impl == 'tma' else ''} gather + "
-                          "ig_fetch_all copy-engine rows)",
-                "bound": "host_link", "achieved": fetch_gbs, "peak": link_peak["gbs"],
-                "peak_source": link_peak["source"], "unit": "GB/s",
-                "frac": (fetch_gbs / link_peak["gbs"]) if fetch_gbs else None,
-                "traffic": per_launch * tr["fetch"]["sysmem_per_payload"] if tr else None,
-                "traffic_pcie": per_launch * tr["fetch"]["pcie_per_payload"] if tr else None,
-                "traffic_source": ("host-memory bytes read (and raw PCIe bytes) per algorithmic byte from "
-                                   "the committed ncu capture profiles/r01_traffic.json, scaled to this "
-                                   "run's average launch") if tr else None,
-                "bytes_per_launch": per_launch,
-                "step_share": f_ms / ms if ms else None}
+        ms_inst = stats.get("instrumented_ms_per_step", ms / a.steps) * a.steps   # stats' own steps
+        link_roof = _link_roofline(stats, link_peak, tr, ms_inst, a)
+        f_bytes = link_roof.pop("_bytes")
+        # the step's dominant kernel kind (device time inside the timed steps)
+        kinds = {k: v["ms"] for k, v in stats.items() if isinstance(v, dict) and v.get("ms")}
+        fetch_ms = sum(v for k, v in kinds.items() if k.startswith("fetch"))
+        other = {k: v for k, v in kinds.items() if not k.startswith("fetch")}
+        top = max(other, key=other.get) if other else None
+        if top is not None and other[top] > fetch_ms:
+            st = stats[top]
+            roof = {"kernel": {"dense": f"dense projections ({_config(a)['dense']})",
+                               "rehearse": "ig_rehearse_count", "attend": "ig_attend",
+                               "select": "ig_select"}.get(top, top),
+                    "bound": "hbm", "achieved": st["gbs"], "peak": hbm_peak,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)", "unit": "GB/s",
+                    "frac": st["gbs"] / hbm_peak if st["gbs"] else None,
+                    "traffic": (st["bytes"] / st["launches"] * tr[top]["dram_per_algorithmic"]
+                                if tr and top in tr else None),
+                    "traffic_source": ("dram bytes per algorithmic byte from the committed ncu capture "
+                                       "profiles/r01_traffic.json") if tr and top in tr else None,
+                    "bytes_per_launch": st["bytes"] / st["launches"],
+                    "ms_per_launch": st["ms"] / st["launches"], "launches": st["launches"],
+                    "step_share": st["ms"] / ms_inst if ms_inst else None,
+                    "how": "CUDA events around every launch on the compute stream, timed steps"}
+        else:
+            roof = link_roof
         hbm = {}
         for k in ("rehearse_count", "attend", "select", "dense_ffn_in"):   # alone: own roofline
             if k in iso:
@@ -373,7 +412,8 @@ def run_b200(a) -> None:
                 "dtype": "f32 compute (rehearsal, attention, dense), f16 host KV pool",
                 "data": ("synthetic: random-init OPT-13B-shaped weights (reference recipe, torch RNG), "
                          "GPU-SVD skew, N(0,1) prompts, GPU prefill"),
-                "config": _config(a), "roofline": roof, "roofline_hbm": hbm,
+                "config": _config(a), "roofline": roof, "roofline_link": link_roof,
+                "roofline_hbm": hbm,
                 "kernel_stats": stats, "clocks": clk.summary(),
                 "e2e": {"value": tok / (e2e_ms / 1000.0), "unit": UNIT,
                         "h2d_bytes_per_step": a.batch * spec.model_dim * 4,
@@ -381,7 +421,16 @@ def run_b200(a) -> None:
                 "gpu_launches": launches, "setup_s": setup_s,
                 "link_bytes_per_step": {"reference_accounted": _ref_bytes(stats, eng, a.steps),
                                         "moved": f_bytes / a.steps}}
-        if var_stats is not None:
+        if var_stats is not None and var_kind == "refetch":
+            vroof = _link_roofline(var_stats, link_peak, tr, var_ms, a)
+            line["variant_refetch"] = {
+                "value": tok / (var_ms / 1000.0), "unit": UNIT, "ms_per_step": var_ms / a.steps,
+                "note": "same engine and state with resident selection off: every selected row "
+                        "(and all of layer 0) fetched from the host pool every step -- the "
+                        "reference's data movement, host-link bound",
+                "link_bytes_per_step_moved": vroof.pop("_bytes") / a.steps,
+                "roofline": vroof, "kernel_stats": var_stats}
+        elif var_stats is not None:
             vk = [k for k in ("fetch_gather", "fetch_all_ce") if k in var_stats]
             line["variant_layer0_in_hbm"] = {
                 "value": tok / (var_ms / 1000.0), "unit": UNIT, "ms_per_step": var_ms / a.steps,
@@ -398,6 +447,28 @@ def run_b200(a) -> None:
     eng.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def _link_roofline(stats, link_peak, tr, ms, a) -> dict:
+    """Host-link roofline of the fetch stream (gather + copy-engine rows)."""
+    keys = [k for k in ("fetch_gather", "fetch_slots", "fetch_all_ce") if k in stats]
+    f_bytes = sum(stats[k]["bytes"] for k in keys)
+    f_ms = sum(stats[k]["ms"] for k in keys)
+    f_launch = sum(stats[k]["launches"] for k in keys)
+    gbs = f_bytes / (f_ms * 1e6) if f_ms else None
+    per_launch = f_bytes / max(f_launch, 1)
+    fr = tr.get("fetch") if tr else None
+    return {"kernel": ("fetch (" + " + ".join(keys) + ")") if keys else "fetch",
+            "bound": "host_link", "achieved": gbs, "peak": link_peak["gbs"],
+            "peak_source": link_peak["source"], "unit": "GB/s",
+            "frac": (gbs / link_peak["gbs"]) if gbs else None,
+            "traffic": per_launch * fr["sysmem_per_payload"] if fr else None,
+            "traffic_pcie": per_launch * fr["pcie_per_payload"] if fr else None,
+            "traffic_source": ("host-memory bytes read (and raw PCIe bytes) per algorithmic byte from "
+                               "the committed ncu capture profiles/r01_traffic.json, scaled to this "
+                               "run's average launch") if fr else None,
+            "bytes_per_launch": per_launch, "launches": f_launch,
+            "step_share": f_ms / ms if ms else None, "_bytes": f_bytes}
 
 
 def _traffic_ratios():

@@ -226,6 +226,15 @@ int ig_sgemm_rows(const float* X, int ldx, const float* W, int ldw, float* Y, in
                   const float* R, int ldr, int M, int N, int K, int ksplit, int epilogue,
                   float* workspace, size_t workspace_floats, int32_t* tickets, void* stream);
 
+/* Same contract on the tensor cores: 3xTF32 split precision (x = x_hi + x_lo,
+ * w = w_hi + w_lo, each part TF32-rounded; x.w = x_hi.w_hi + x_hi.w_lo +
+ * x_lo.w_hi with f32 accumulation) -- f32-level accuracy, not bit-identical
+ * to ig_sgemm_rows.  Same workspace / ticket / ksplit rules.               */
+int ig_sgemm_tc_ksplit(int M, int N, int K);
+int ig_sgemm_tc(const float* X, int ldx, const float* W, int ldw, float* Y, int ldy,
+                const float* R, int ldr, int M, int N, int K, int ksplit, int epilogue,
+                float* workspace, size_t workspace_floats, int32_t* tickets, void* stream);
+
 /* ---- step bookkeeping -------------------------------------------------- */
 /* s_len = min(s_len + 1, limit), seq += 2, step += 1 (engine.py:377-378). */
 int ig_step_advance(ig_step_state* st, void* stream);

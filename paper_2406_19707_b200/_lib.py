@@ -55,6 +55,8 @@ _SIGS = {
     "ig_memcpy2d": [_P, _SZ, _P, _SZ, _SZ, _SZ, _P],
     "ig_sgemm_rows_ksplit": [_I, _I, _I],
     "ig_sgemm_rows": [_P, _I, _P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _I, _P, _SZ, _P, _P],
+    "ig_sgemm_tc_ksplit": [_I, _I, _I],
+    "ig_sgemm_tc": [_P, _I, _P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _I, _P, _SZ, _P, _P],
     "ig_step_advance": [_P, _P],
     "ig_layernorm": [_P, _P, _P, _F, _I, _I, _P, _P],
 }

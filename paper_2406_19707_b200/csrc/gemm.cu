@@ -13,6 +13,8 @@
 // (ticket) sums them in fixed split order and applies the epilogue -- the
 // result is deterministic.  IEEE f32 throughout (no TF32: x_a feeds the
 // rehearsal, whose index parity needs f32).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace ig {
@@ -28,6 +30,64 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool va
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem), "r"(n)
                : "memory");
 }
+
+// Per-thread stage loader with the addressing hoisted out of the K loop:
+// thread tid copies the 16-B vectors (row w + 8i, column quad lane) of every
+// 32-row weight chunk, i = 0..3, and (tid < MT*8) vector tid of the x slice.
+// A whole chunk needs one pointer increment per vector; only the last chunk
+// of K (rows >= K) and a ragged column tile take the zero-filling path.
+template <int MT>
+struct StageLoader {
+  const char* wp;        // this thread's first W vector of chunk 0
+  const char* xp;        // this thread's x vector of chunk 0 (nullptr: none)
+  size_t wrow8;          // bytes between rows r and r + 8
+  size_t wchunk;         // bytes between chunks
+  int krow0, xk, K;      // first row of chunk 0, x column of this thread, K
+  bool colok, xok;
+  uint32_t wdst, xdst;   // shared offsets within a stage (bytes)
+
+  __device__ void init(const float* W, int ldw, const float* X, int ldx, int M, int N, int K_,
+                       int c0, int ncol0, int wpitch, int xpitch, int kWsFloats) {
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    K = K_;
+    krow0 = c0 * kGemmKT + w;
+    colok = ncol0 + lane * 4 < N;
+    wp = reinterpret_cast<const char*>(W + (size_t)krow0 * ldw + ncol0 + lane * 4);
+    wrow8 = (size_t)8 * ldw * sizeof(float);
+    wchunk = (size_t)kGemmKT * ldw * sizeof(float);
+    wdst = (uint32_t)((w * wpitch + lane * 4) * sizeof(float));
+    const int m = tid / (kGemmKT / 4), k4 = tid % (kGemmKT / 4);
+    xok = tid < MT * (kGemmKT / 4) && m < M;
+    xk = c0 * kGemmKT + k4 * 4;
+    xp = reinterpret_cast<const char*>(X + (size_t)(m < M ? m : 0) * ldx + xk);
+    xdst = (uint32_t)((kWsFloats + m * xpitch + k4 * 4) * sizeof(float));
+    (void)lane;
+  }
+  // chunk c (relative to c0) into the stage at shared address `base`
+  __device__ __forceinline__ void load(int c, uint32_t base, int wpitch) const {
+    const char* src = wp + (size_t)c * wchunk;
+    const int k = krow0 + c * kGemmKT;
+    if (colok && k + 24 < K) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(base + wdst + i * 8 * wpitch * 4),
+                     "l"(src + i * wrow8) : "memory");
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const bool ok = colok && k + 8 * i < K;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(base + wdst + i * 8 * wpitch * 4),
+                     "l"(ok ? src + i * wrow8 : wp), "r"(ok ? 16 : 0) : "memory");
+      }
+    }
+    if (tid_has_x()) {
+      const bool ok = xok && xk + c * kGemmKT < K;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(base + xdst),
+                   "l"(ok ? xp + (size_t)c * kGemmKT * sizeof(float) : xp), "r"(ok ? 16 : 0) : "memory");
+    }
+  }
+  __device__ __forceinline__ bool tid_has_x() const { return threadIdx.x < MT * (kGemmKT / 4); }
+};
 
 // Stage layout: Ws[stage][KT][128] then Xs[stage][MT][KT] (floats).
 template <int MT>
@@ -48,27 +108,10 @@ sgemm_rows_kernel(const float* __restrict__ X, int ldx, const float* __restrict_
   const int c0 = ks * cper, c1 = min(chunks_all, c0 + cper);
   const int nch = max(0, c1 - c0);
 
-  auto load_stage = [&](int c, int st) {
-    float* ws_ = smem + st * kStage;
-    float* xs_ = ws_ + kWs;
-    const int kb = (c0 + c) * kGemmKT;
-    // W: KT x 128 floats = KT*32 float4, 8 per thread
-#pragma unroll
-    for (int i = 0; i < kGemmKT * 32 / (kGemmWarps * 32); ++i) {
-      const int f = tid + i * kGemmWarps * 32;
-      const int r = f >> 5, c4 = f & 31;
-      const int k = kb + r, n = ncol0 + c4 * 4;
-      const bool ok = k < K && n < N;
-      cp_async16(ws_ + r * kGemmTileN + c4 * 4, ok ? (const void*)(W + (size_t)k * ldw + n) : (const void*)W, ok);
-    }
-    // X: MT x KT floats = MT*KT/4 float4
-    for (int f = tid; f < MT * kGemmKT / 4; f += kGemmWarps * 32) {
-      const int m = f / (kGemmKT / 4), k4 = f % (kGemmKT / 4);
-      const int k = kb + k4 * 4;
-      const bool ok = m < M && k < K;
-      cp_async16(xs_ + m * kGemmKT + k4 * 4, ok ? (const void*)(X + (size_t)m * ldx + k) : (const void*)X, ok);
-    }
-  };
+  StageLoader<MT> ld;
+  ld.init(W, ldw, X, ldx, M, N, K, c0, ncol0, kGemmTileN, kGemmKT, kWs);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  auto load_stage = [&](int c, int st) { ld.load(c, sbase + st * kStage * 4, kGemmTileN); };
 
   float acc[MT][4];
 #pragma unroll
@@ -171,6 +214,168 @@ int launch_sgemm(const float* X, int ldx, const float* W, int ldw, float* Y, int
   return IG_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Tensor-core variant: 3xTF32 split precision on mma.sync m16n8k8.  Every f32
+// operand is split into a TF32 head and a tail (v = hi + lo exactly; hi is v
+// rounded to TF32 by integer add + mask, lo = v - hi, which the tensor core
+// reads truncated to TF32); x.w = x_hi.w_hi + (x_hi.w_lo + x_lo.w_hi) with the
+// two tail products in their own accumulator -- f32-level accuracy (the
+// neglected terms are ~2^-21 relative).
+//
+// Weights stream through the same 16-B cp.async pipeline as sgemm_rows_kernel
+// (StageLoader: per-thread addressing hoisted out of the K loop).  TMA 1-D
+// bulk copies of the 512-B rows were measured slower (1.9 TB/s: the TMA unit
+// serves ~one request per ~46 cycles per SM, too few bytes per request).
+// CTA = 128 columns x one K slice (fixed-order
+// split-K merge as sgemm_rows_kernel); each warp owns 16 columns over the
+// whole slice, so no cross-warp reduction.  Shared rows are padded (W: 136
+// floats, X: 36) so a warp's fragment loads hit 32 distinct banks.
+// ---------------------------------------------------------------------------
+constexpr int kTcWPitch = kGemmTileN + 8;    // 136
+constexpr int kTcXPitch = kGemmKT + 4;       // 36
+
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;   // round half away, 10-bit mantissa
+  lo = __float_as_uint(x - __uint_as_float(hi));        // exact remainder
+}
+__device__ __forceinline__ void mma_tf32(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int MTILES, int STAGES>   // 16-row M tiles (M <= 16 * MTILES), pipeline depth
+__global__ void __launch_bounds__(kGemmWarps * 32, (MTILES == 1 ? (STAGES <= 3 ? 3 : 2) : 1))
+sgemm_tc_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ W, int ldw,
+                float* __restrict__ Y, int ldy, const float* __restrict__ R, int ldr, int M, int N,
+                int K, int ksplit, int epilogue, float* __restrict__ ws,
+                int32_t* __restrict__ tickets) {
+  extern __shared__ __align__(128) float smem[];
+  constexpr int MT = 16 * MTILES;
+  constexpr int kWs = kGemmKT * kTcWPitch, kXs = MT * kTcXPitch, kStage = kWs + kXs;
+  __shared__ int last;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int tile = blockIdx.x, ks = blockIdx.y;
+  const int ncol0 = tile * kGemmTileN;
+  const int chunks_all = (K + kGemmKT - 1) / kGemmKT;
+  const int cper = (chunks_all + ksplit - 1) / ksplit;
+  const int c0 = ks * cper, c1 = min(chunks_all, c0 + cper);
+  const int nch = max(0, c1 - c0);
+
+  StageLoader<MT> ld;
+  ld.init(W, ldw, X, ldx, M, N, K, c0, ncol0, kTcWPitch, kTcXPitch, kWs);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  auto load_stage = [&](int c, int st) { ld.load(c, sbase + st * kStage * 4, kTcWPitch); };
+
+  float big[MTILES][2][4], small[MTILES][2][4], small2[MTILES][2][4];
+#pragma unroll
+  for (int mt = 0; mt < MTILES; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) big[mt][nt][i] = small[mt][nt][i] = small2[mt][nt][i] = 0.f;
+
+#pragma unroll
+  for (int i = 0; i < STAGES - 1; ++i) {
+    if (i < nch) load_stage(i, i);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  const int wn = w * 16;                       // my 16 columns of the tile
+  for (int c = 0; c < nch; ++c) {
+    const int st = c % STAGES;
+    asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 2) : "memory");
+    __syncthreads();                           // stage c landed; stage c-1 fully consumed
+    const int nx = c + STAGES - 1;
+    if (nx < nch) load_stage(nx, nx % STAGES);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const float* ws_ = smem + st * kStage;
+    const float* xs_ = ws_ + kWs;
+#pragma unroll
+    for (int k8 = 0; k8 < kGemmKT; k8 += 8) {
+      uint32_t ahi[MTILES][4], alo[MTILES][4];
+#pragma unroll
+      for (int mt = 0; mt < MTILES; ++mt) {
+        const float* xr = xs_ + (mt * 16 + g) * kTcXPitch + k8 + t;
+        split_tf32(xr[0], ahi[mt][0], alo[mt][0]);
+        split_tf32(xr[8 * kTcXPitch], ahi[mt][1], alo[mt][1]);
+        split_tf32(xr[4], ahi[mt][2], alo[mt][2]);
+        split_tf32(xr[8 * kTcXPitch + 4], ahi[mt][3], alo[mt][3]);
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const float* wr = ws_ + (k8 + t) * kTcWPitch + wn + nt * 8 + g;
+        uint32_t bhi0, blo0, bhi1, blo1;
+        split_tf32(wr[0], bhi0, blo0);
+        split_tf32(wr[4 * kTcWPitch], bhi1, blo1);
+#pragma unroll
+        for (int mt = 0; mt < MTILES; ++mt) {
+          mma_tf32(small[mt][nt], alo[mt], bhi0, bhi1);
+          mma_tf32(small2[mt][nt], ahi[mt], blo0, blo1);
+          mma_tf32(big[mt][nt], ahi[mt], bhi0, bhi1);
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  const size_t tile_elems = (size_t)M * kGemmTileN;
+  float* part = ws + ((size_t)tile * ksplit + ks) * tile_elems;
+#pragma unroll
+  for (int mt = 0; mt < MTILES; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int col = wn + nt * 8 + 2 * t;
+      const int r0 = mt * 16 + g, r1 = r0 + 8;
+      if (r0 < M)
+        *reinterpret_cast<float2*>(part + (size_t)r0 * kGemmTileN + col) =
+            make_float2(big[mt][nt][0] + (small[mt][nt][0] + small2[mt][nt][0]),
+                        big[mt][nt][1] + (small[mt][nt][1] + small2[mt][nt][1]));
+      if (r1 < M)
+        *reinterpret_cast<float2*>(part + (size_t)r1 * kGemmTileN + col) =
+            make_float2(big[mt][nt][2] + (small[mt][nt][2] + small2[mt][nt][2]),
+                        big[mt][nt][3] + (small[mt][nt][3] + small2[mt][nt][3]));
+    }
+  if (ksplit == 1) {
+    __syncthreads();
+  } else {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(tickets + tile, 1) == ksplit - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+  }
+  const float* tp = ws + (size_t)tile * ksplit * tile_elems;
+  for (int e = tid; e < M * kGemmTileN; e += blockDim.x) {
+    const int m = e / kGemmTileN, n = ncol0 + (e % kGemmTileN);
+    if (n >= N) continue;
+    float s = 0.f;
+    for (int i = 0; i < ksplit; ++i) s += __ldcg(tp + (size_t)i * tile_elems + e);
+    if (epilogue == 1) s = fmaxf(s, 0.f);
+    else if (epilogue == 2) s = __fadd_rn(R[(size_t)m * ldr + n], s);
+    Y[(size_t)m * ldy + n] = s;
+  }
+  if (tid == 0 && ksplit > 1) tickets[tile] = 0;
+}
+
+template <int MTILES, int STAGES>
+int launch_sgemm_tc(const float* X, int ldx, const float* W, int ldw, float* Y, int ldy,
+                    const float* R, int ldr, int M, int N, int K, int ksplit, int epilogue,
+                    float* ws, int32_t* tickets, cudaStream_t s) {
+  const int tiles = (N + kGemmTileN - 1) / kGemmTileN;
+  const size_t smem =
+      (size_t)STAGES * (kGemmKT * kTcWPitch + 16 * MTILES * kTcXPitch) * sizeof(float);
+  IG_CUDA_STATUS(cudaFuncSetAttribute(sgemm_tc_kernel<MTILES, STAGES>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  sgemm_tc_kernel<MTILES, STAGES><<<dim3(tiles, ksplit), kGemmWarps * 32, smem, s>>>(
+      X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, ws, tickets);
+  IG_LAUNCH_STATUS();
+  return IG_OK;
+}
+
 }  // namespace ig
 
 extern "C" int ig_sgemm_rows_ksplit(int M, int N, int K) {
@@ -216,4 +421,42 @@ extern "C" int ig_sgemm_rows(const float* X, int ldx, const float* W, int ldw, f
   if (M <= 8) return launch_sgemm<8>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
   if (M <= 16) return launch_sgemm<16>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
   return launch_sgemm<32>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
+}
+
+extern "C" int ig_sgemm_tc_ksplit(int M, int N, int K) {
+  // Measured (tools/gemm_probe.py --ksplit all, C3 shapes, profiles/r01b_gemm_probe.jsonl):
+  // ~1900 CTAs (>= 4 waves of 3 CTAs/SM) beat the wave-filling rule of
+  // ig_sgemm_rows_ksplit by 5-15%; more than 16 splits only adds merge traffic.
+  (void)M;
+  const int tiles = (N + ig::kGemmTileN - 1) / ig::kGemmTileN;
+  const int chunks = (K + ig::kGemmKT - 1) / ig::kGemmKT;
+  int ks = (1920 + tiles - 1) / tiles;
+  if (ks > 16) ks = 16;
+  if (ks > chunks / 4) ks = chunks / 4;
+  return ks < 1 ? 1 : ks;
+}
+
+extern "C" int ig_sgemm_tc(const float* X, int ldx, const float* W, int ldw, float* Y, int ldy,
+                           const float* R, int ldr, int M, int N, int K, int ksplit, int epilogue,
+                           float* workspace, size_t workspace_floats, int32_t* tickets,
+                           void* stream) {
+  using namespace ig;
+  if (!X || !W || !Y || !workspace || !tickets || M < 1 || M > 32 || N < 4 || (N & 3) || K < 4 ||
+      (K & 3) || ldx < K || (ldx & 3) || ldw < N || (ldw & 3) || ldy < N || ksplit < 1 ||
+      epilogue < 0 || epilogue > 2 || (epilogue == 2 && (!R || ldr < N)))
+    return IG_EINVAL;
+  if (((uintptr_t)X & 15) || ((uintptr_t)W & 15)) return IG_EINVAL;   // 16-B vectors
+  const int tiles = (N + kGemmTileN - 1) / kGemmTileN;
+  if ((size_t)tiles * ksplit * M * kGemmTileN > workspace_floats) return IG_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  static const int stages = [] {
+    const char* v = getenv("IG_TC_STAGES");   // tuning sweeps only
+    return v ? atoi(v) : 3;
+  }();
+  if (M <= 16) {
+    if (stages == 4)
+      return launch_sgemm_tc<1, 4>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
+    return launch_sgemm_tc<1, 3>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
+  }
+  return launch_sgemm_tc<2, 4>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
 }

@@ -171,7 +171,7 @@ class DecodeEngine:
     def __init__(self, model, config: RunConfig, *, max_steps: int | None = None,
                  pool_dtype: str = "f16", device=None, group=None, fetch_ctas: int = 32,
                  fetch_threads: int = 32, fetch_priority: int = 0, hbm_layers: int = 0,
-                 fetch_impl: str = "tma", fetch_rows: int = 16, dense: str = "ig",
+                 fetch_impl: str = "tma", fetch_rows: int = 16, dense: str = "tc",
                  cuda_graph: bool = False, resident: bool = False):
         config.validate()
         _lib.load()
@@ -212,8 +212,8 @@ class DecodeEngine:
             raise ValueError("fetch_impl must be 'ldg' or 'tma'")
         self.fetch_impl = fetch_impl
         self.fetch_rows = fetch_rows
-        if dense not in ("ig", "cublas"):
-            raise ValueError("dense must be 'ig' or 'cublas'")
+        if dense not in ("ig", "tc", "cublas"):
+            raise ValueError("dense must be 'ig', 'tc' or 'cublas'")
         self.dense = dense
         self.cuda_graph = cuda_graph
         if cuda_graph and (config.record_selection or config.record_scores):
@@ -295,21 +295,13 @@ class DecodeEngine:
         self.stage_sel = [torch.empty((B, Hg, cap, 2 * d), dtype=T, device=dev)
                           for _ in range(2 if spec_ and not self.resident else 0)]
         if self.resident:
-            Lr = max(L - 1, 1)
-            # zero-filled: a slot never written must not hold NaN bits
-            self.stage_res = torch.zeros((Lr, B, Hg, cap, 2 * d), dtype=T, device=dev)
-            self.slot_id = torch.full((Lr, B, Hg, cap), -1, dtype=i32, device=dev)
-            self.slot_used = torch.zeros((Lr, B, Hg), dtype=i32, device=dev)
-            self.frow = torch.zeros((2, B, Hg, cap), dtype=i32, device=dev)
-            self.fslot = torch.zeros((2, B, Hg, cap), dtype=i32, device=dev)
-            self.fcount = torch.zeros((2, B, Hg), dtype=i32, device=dev)
-            self.moved_rows = torch.zeros(L, dtype=i64, device=dev)
+            self._alloc_resident()
         # skinny-GEMM workspace: the largest ceil(N/128) * ksplit * B * 128 over the projections
         shapes = [(3 * Hg * d, D), (Hg * d, D), (D, Hg * d), (F, D), (D, F)]   # (N, K)
         ws = 0
         self.gemm_ksplit = {}
         for N_, K_ in shapes:
-            ksp = _lib.load().ig_sgemm_rows_ksplit(B, N_, K_)
+            ksp = self._ksplit(B, N_, K_)
             self.gemm_ksplit[(N_, K_)] = ksp
             ws = max(ws, ((N_ + 127) // 128) * ksp * B * 128)
         self.gemm_ws = torch.empty(ws, dtype=f32, device=dev)
@@ -324,6 +316,44 @@ class DecodeEngine:
         self.ev_fetch = [torch.cuda.Event() for _ in range(L)]
         self.ev_att = [torch.cuda.Event() for _ in range(L)]
         self.ev_step = torch.cuda.Event()
+
+    def _alloc_resident(self) -> None:
+        dev, B, L, Hg, d, cap = self.device, self.B, self.L, self.Hg, self.d, self.cap
+        i32 = torch.int32
+        Lr = max(L - 1, 1)
+        # zero-filled: a slot never written must not hold NaN bits
+        self.stage_res = torch.zeros((Lr, B, Hg, cap, 2 * d), dtype=_TORCH_ELT[self.elt], device=dev)
+        self.slot_id = torch.full((Lr, B, Hg, cap), -1, dtype=i32, device=dev)
+        self.slot_used = torch.zeros((Lr, B, Hg), dtype=i32, device=dev)
+        self.frow = torch.zeros((2, B, Hg, cap), dtype=i32, device=dev)
+        self.fslot = torch.zeros((2, B, Hg, cap), dtype=i32, device=dev)
+        self.fcount = torch.zeros((2, B, Hg), dtype=i32, device=dev)
+        self.moved_rows = torch.zeros(L, dtype=torch.int64, device=dev)
+
+    def set_resident(self, on: bool) -> None:
+        """Switch between resident selection and refetching every selected row
+        each step (the reference's data movement); decode state is kept."""
+        on = bool(on)
+        torch.cuda.synchronize(self.device)
+        if on == self.resident:
+            return
+        if on and (self.scheme != "speculative" or self.hbm_layers):
+            raise ValueError("resident needs the speculative scheme and hbm_layers=0")
+        if on:
+            self.stage_sel = []
+            torch.cuda.empty_cache()
+            self._alloc_resident()
+        else:
+            for name in ("stage_res", "slot_id", "slot_used", "frow", "fslot", "fcount", "moved_rows"):
+                delattr(self, name)
+            torch.cuda.empty_cache()
+            self.stage_sel = [torch.empty((self.B, self.Hg, self.cap, 2 * self.d),
+                                          dtype=_TORCH_ELT[self.elt], device=self.device)
+                              for _ in range(2)]
+        self.resident = on
+        self._res_valid = False
+        self._prefetched0 = False
+        self._graph = None
 
     def _set_state(self, s_len: int, seq: int) -> None:
         limit = self.config.pool_limit or 0
@@ -538,14 +568,14 @@ class DecodeEngine:
             self._inst["moved0"] = self.moved_rows.clone()
             self._inst["moved"] = torch.zeros((steps, self.L), dtype=torch.int64, device=self.device)
 
-    def _mark(self, kind: str, li: int, stream, start: bool):
+    def _mark(self, kind: str, li: int, stream, start: bool, nbytes: int | None = None):
         inst = self._inst
         if inst is None or self._graph_mode or inst["k"] >= inst["steps"]:
             return
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(stream)
         if start:
-            inst["ev"].append([inst["k"], kind, li, ev, None])
+            inst["ev"].append([inst["k"], kind, li, ev, None, nbytes])
         else:
             for rec in reversed(inst["ev"]):
                 if rec[1] == kind and rec[2] == li and rec[4] is None:
@@ -564,11 +594,13 @@ class DecodeEngine:
             snap = np.concatenate([inst["moved0"].cpu().numpy()[None], inst["moved"].cpu().numpy()])
             moved = np.diff(snap, axis=0)                 # [step][layer] rows fetched
         out = {}
-        for k, kind, li, e0, e1 in inst["ev"]:
+        for k, kind, li, e0, e1, nb in inst["ev"]:
             if e1 is None:
                 continue
             s = inst["s"][k]
-            if kind == "fetch" and moved is not None and li >= 1:
+            if nb is not None:
+                nbytes = nb                               # dense: 4 (K N + M K + M N)
+            elif kind == "fetch" and moved is not None and li >= 1:
                 nbytes = int(moved[k, li]) * rb           # resident: rows that entered the set
             elif kind == "fetch":
                 rows = B * s if (li == 0 or self.scheme == "full") else int(n_hist[k, li].sum())
@@ -660,6 +692,10 @@ class DecodeEngine:
         return out
 
     # ----------------------------------------------------------------- decode
+    def _ksplit(self, M, N, K) -> int:
+        lib = _lib.load()
+        return lib.ig_sgemm_tc_ksplit(M, N, K) if self.dense == "tc" else lib.ig_sgemm_rows_ksplit(M, N, K)
+
     def _gemm(self, X, W, Y, cs, epilogue: int = 0, R=None) -> None:
         """Y = X @ W (+ ReLU / + R) on the compute stream."""
         M, K = X.shape
@@ -672,11 +708,15 @@ class DecodeEngine:
                 if epilogue == 1:
                     Y.relu_()
             return
-        ksp = self.gemm_ksplit.get((N, K)) or _lib.load().ig_sgemm_rows_ksplit(M, N, K)
-        _lib.call("ig_sgemm_rows", X.data_ptr(), X.stride(0), W.data_ptr(), W.stride(0),
+        ksp = self.gemm_ksplit.get((N, K)) or self._ksplit(M, N, K)
+        if self._inst is not None:
+            self._mark("dense", -1, self.compute, True, 4 * (K * N + M * K + M * N))
+        _lib.call("ig_sgemm_tc" if self.dense == "tc" else "ig_sgemm_rows", X.data_ptr(), X.stride(0), W.data_ptr(), W.stride(0),
                   Y.data_ptr(), Y.stride(0), _lib.ptr(R), R.stride(0) if R is not None else 0,
                   M, N, K, ksp, epilogue, self.gemm_ws.data_ptr(), self.gemm_ws.numel(),
                   self.gemm_tickets.data_ptr(), cs)
+        if self._inst is not None:
+            self._mark("dense", -1, self.compute, False)
 
     def _issue_full_fetch(self, li: int, s: int, stage: torch.Tensor) -> None:
         self._mark("fetch", li, self.fetch_stream, True)

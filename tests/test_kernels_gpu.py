@@ -226,9 +226,11 @@ def test_blocked_causal_prefill_attention_matches_oracle():
 @pytest.mark.parametrize("M,N,K", [(1, 128, 64), (5, 260, 100), (8, 512, 5120), (16, 5120, 5120),
                                    (17, 1024, 2048), (32, 384, 4096), (16, 20480, 512)])
 @pytest.mark.parametrize("epilogue", [0, 1, 2])
-def test_sgemm_rows_vs_float64(M, N, K, epilogue):
-    """ig_sgemm_rows (dense projections) vs float64, every M template, ragged
-    tiles, split-K, fused epilogues; bit-identical on repeat (deterministic)."""
+@pytest.mark.parametrize("fn", ["ig_sgemm_rows", "ig_sgemm_tc"])
+def test_sgemm_rows_vs_float64(M, N, K, epilogue, fn):
+    """ig_sgemm_rows (dense projections, CUDA-core f32) and ig_sgemm_tc (3xTF32
+    tensor cores) vs float64, every M template, ragged tiles, split-K, fused
+    epilogues; bit-identical on repeat (deterministic)."""
     import torch
     from paper_2406_19707_b200 import _lib
     lib = _lib.load()
@@ -243,7 +245,7 @@ def test_sgemm_rows_vs_float64(M, N, K, epilogue):
     outs = []
     for _ in range(2):
         Y = torch.empty(M, N, device="cuda")
-        _lib.call("ig_sgemm_rows", X.data_ptr(), K, W.data_ptr(), W.stride(0), Y.data_ptr(), N,
+        _lib.call(fn, X.data_ptr(), K, W.data_ptr(), W.stride(0), Y.data_ptr(), N,
                   R.data_ptr() if epilogue == 2 else None, N if epilogue == 2 else 0, M, N, K, ksp,
                   epilogue, ws.data_ptr(), ws.numel(), tk.data_ptr(), _lib.stream_handle())
         outs.append(Y.clone())

@@ -146,13 +146,16 @@ SPEC_RUNS = sorted(r for r in RUNS if RUNS[r]["scheme"] == "speculative")
 
 @pytest.mark.parametrize("rname", SPEC_RUNS)
 @pytest.mark.parametrize("mname", ["m64", "m256"])
-def test_resident_engine_matches_oracle(mname, rname):
+@pytest.mark.parametrize("dense", ["ig", "tc"])
+def test_resident_engine_matches_oracle(mname, rname, dense):
+    """dense="tc": the projections on 3xTF32 tensor cores -- still every
+    selection identical to the oracle's (f32-level x_a)."""
     from paper_2406_19707_b200 import DecodeEngine
     _, sk = models(mname)
     ocfg = run_config(rname, record_selection=True)
     sessions = oracle_sessions(sk, ocfg)
     eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg), copy.deepcopy(sessions), pool_dtype="f32",
-                                     resident=True)
+                                     resident=True, dense=dense)
     try:
         ref_out, ref_recs = oracle_decode(sessions, ocfg.gen_len)
         got = np.stack([eng.x.cpu().numpy()] + [eng.decode_step().cpu().numpy()
