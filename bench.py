@@ -59,7 +59,8 @@ def _args():
     ap.add_argument("--fetch-impl", default="tma", choices=["ldg", "tma"])
     ap.add_argument("--fetch-rows", type=int, default=16, help="TMA rows per warp batch")
     ap.add_argument("--dense", default="tc", choices=["ig", "tc", "cublas"])
-    ap.add_argument("--cuda-graph", action="store_true", help="replay a captured decode step")
+    ap.add_argument("--no-cuda-graph", dest="cuda_graph", action="store_false",
+                    help="launch every kernel eagerly instead of replaying a captured decode step")
     ap.add_argument("--no-resident", dest="resident", action="store_false",
                     help="refetch every selected row each step (the reference's data movement) "
                          "instead of keeping each layer's fetched set resident in HBM")
@@ -290,9 +291,9 @@ def run_b200(a) -> None:
     launches = _lib.launches - launches0
     if a.cuda_graph:   # one eager step's launches are replayed per step
         launches = eng.graph_launches * a.steps
-        stats = _graph_stats(eng, a.steps)
-    else:
-        # -------- per-kernel CUDA events over another K steps (not the headline)
+    # -------- per-kernel CUDA events over another K eager steps (not the headline)
+    eng.cuda_graph = False
+    try:
         eng.instrument(a.steps)
         i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         i0.record(cur)
@@ -303,6 +304,8 @@ def run_b200(a) -> None:
         stats = eng.kernel_stats()
         stats["instrumented_ms_per_step"] = i0.elapsed_time(i1) / a.steps
         eng._inst = None
+    finally:
+        eng.cuda_graph = a.cuda_graph
     iso = eng.isolated_kernel_times(li=eng.L // 2) if eng.L > 2 else {}
     # -------- end-to-end: public API with host input/output rows each step
     x_host = torch.empty((a.batch, spec.model_dim), dtype=torch.float32).pin_memory()
@@ -319,8 +322,9 @@ def run_b200(a) -> None:
     var_ms = 0.0
     var_stats = None
     var_kind = None
-    if not a.no_variant and a.resident and not a.cuda_graph:
+    if not a.no_variant and a.resident:
         var_kind = "refetch"
+        eng.cuda_graph = False          # the variant is timed eagerly, with its kernel events
         eng.set_resident(False)
         for _ in range(2):
             eng.decode_step()

@@ -571,17 +571,315 @@ attend512_tma_kernel(const float* __restrict__ q, int ldq, const float* __restri
   if (threadIdx.x == 0) tickets[bh] = 0;
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core 512-B-row path (default for d = 128 with a 2-byte pool).
+// The per-row CUDA-core work of attend512_kernel (f16 -> f32 unpack, 16
+// FMAs and 5 shuffles per row and lane) bounded it at ~0.44 of HBM; here both
+// products run on mma.sync m16n8k16 over 16-row tiles:
+//   scores  S[16 rows x 8] = K_tile[16 x 128] . Qm[128 x 8], Qm's columns
+//           0..NS-1 = the f32 query split into NS parts exactly representable
+//           in T (q = q0 + q1 (+ q2)), so S[r][0] + .. + S[r][NS-1] is q.k to
+//           ~2^-22 (f16: NS = 2, bf16: NS = 3);
+//   output  O[16 x 128] += Pm[16 x 16 rows] . V_tile[16 x 128], Pm's rows
+//           0..NS-1 = the split softmax weights p of the tile's 16 rows.
+// f32 accumulation throughout; scores are (q.k) / float32(sqrt(d)) as in
+// model.py:174 and exp is expf.  Rows stream into a per-warp shared-memory
+// ring by cp.async (16-B chunk c of row r stored at chunk c ^ (r & 7), so the
+// ldmatrix phases are conflict-free); a warp owns every 4th 16-row tile of
+// the CTA's chunk and keeps its own online softmax; warps and chunks merge in
+// fixed order as in attend512_kernel (deterministic).
+// ---------------------------------------------------------------------------
+constexpr int kMmaWarps = 4;
+constexpr int kMmaTPW = 8;                                  // tiles per warp
+constexpr int kMmaChunk = kMmaWarps * kMmaTPW * 16;          // 512 rows per CTA
+constexpr int kMmaTileBytes = 16 * 512;
+
+template <typename T> struct MmaT;
+template <> struct MmaT<__half> {
+  static constexpr int NS = 2;
+  __device__ static uint32_t pack(float lo_elem, float hi_elem) {
+    __half2 h = __floats2half2_rn(lo_elem, hi_elem);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  __device__ static float round(float x) { return __half2float(__float2half_rn(x)); }
+  __device__ static void mma(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  }
+};
+template <> struct MmaT<__nv_bfloat16> {
+  static constexpr int NS = 3;
+  __device__ static uint32_t pack(float lo_elem, float hi_elem) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo_elem, hi_elem);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  __device__ static float round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+  __device__ static void mma(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  }
+};
+
+// part `g` of the exact split x = x0 + x1 (+ x2), each part representable in T
+template <typename T>
+__device__ __forceinline__ float split_part(float x, int g) {
+  const float x0 = MmaT<T>::round(x);
+  const float r1 = x - x0;
+  const float x1 = MmaT<T>::round(r1);
+  if (g == 0) return x0;
+  if (g == 1) return x1;
+  if (MmaT<T>::NS > 2 && g == 2) return MmaT<T>::round(r1 - x1);
+  return 0.f;
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t* r) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+
+template <typename T, int RING>
+__global__ void __launch_bounds__(kMmaWarps * 32, 2)
+attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_cur,
+                     const float* __restrict__ v_cur, int ldkv, const T* __restrict__ stage,
+                     const int32_t* __restrict__ idx, const int32_t* __restrict__ n_in,
+                     const int32_t* __restrict__ rows_bh, const int32_t* __restrict__ pos_in,
+                     const ig_step_state* __restrict__ st, int Hg, int cap, float sqrt_d,
+                     int max_chunks, float* __restrict__ partial, int32_t* __restrict__ tickets,
+                     float* __restrict__ out, int ldo) {
+  constexpr int d = 128, NS = MmaT<T>::NS;
+  extern __shared__ __align__(128) uint8_t att_ring[];       // [warps][RING][16 rows][512 B]
+  __shared__ float wm[kMmaWarps], wl[kMmaWarps];
+  __shared__ float wacc[kMmaWarps][d];
+  __shared__ int last;
+  const int b = blockIdx.z, h = blockIdx.y, c = blockIdx.x;
+  const size_t bh = (size_t)b * Hg + h;
+  const int rows = att_rows(rows_bh, n_in, st, b, bh);
+  const int nchunks = max(1, (rows + kMmaChunk - 1) / kMmaChunk);
+  if (c >= nchunks) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int pos = pos_in[bh];
+  const int r0 = c * kMmaChunk, r1 = min(rows, r0 + kMmaChunk);
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(stage + bh * (size_t)cap * 2 * d);
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(att_ring) + w * RING * kMmaTileBytes;
+
+  // query split into NS parts: B fragments of the 8 k16-steps (column g < NS)
+  uint32_t bq[8][2];
+  {
+    const float* qr = q + (size_t)b * ldq + (size_t)h * d;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int k0 = kk * 16 + 2 * t;
+      bq[kk][0] = MmaT<T>::pack(split_part<T>(qr[k0], g), split_part<T>(qr[k0 + 1], g));
+      bq[kk][1] = MmaT<T>::pack(split_part<T>(qr[k0 + 8], g), split_part<T>(qr[k0 + 9], g));
+      if (g >= NS) bq[kk][0] = bq[kk][1] = 0u;
+    }
+  }
+  float m = -INFINITY, l = 0.f;
+  float acc[16][4];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+
+  // tile j of this warp: rows [tb, tb + 16), tb = r0 + (j * warps + w) * 16
+  int ids[kMmaTPW][2];
+  auto issue = [&](int j) {
+    const int tb = r0 + (j * kMmaWarps + w) * 16;
+    const uint32_t slot = ring + (j % RING) * kMmaTileBytes;
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr) {
+      const int r = tb + rr;
+      const bool ok = r < r1;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                   ::"r"(slot + rr * 512 + ((lane ^ (rr & 7)) << 4)),
+                   "l"(src + (size_t)(ok ? r : r0) * 512 + lane * 16), "r"(ok ? 16 : 0)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int r = tb + g + 8 * u;
+      ids[j][u] = r < r1 ? (idx ? idx[bh * cap + r] : r) : -1;
+    }
+  };
+  int ntiles = 0;
+#pragma unroll
+  for (int j = 0; j < kMmaTPW; ++j) ntiles += (r0 + (j * kMmaWarps + w) * 16 < r1) ? 1 : 0;
+
+#pragma unroll
+  for (int j = 0; j < RING - 1; ++j)
+    if (j < ntiles) issue(j);
+#pragma unroll
+  for (int j = 0; j < kMmaTPW; ++j) {
+    if (j >= ntiles) break;
+    if (j + RING - 1 < ntiles) {
+      issue(j + RING - 1);
+      asm volatile("cp.async.wait_group %0;" ::"n"(RING - 1) : "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncwarp();
+    const uint32_t slot = ring + (j % RING) * kMmaTileBytes;
+    // S = K . Qm (two accumulators: half-length dependency chains)
+    float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    const int lr = lane & 15, lh = lane >> 4;
+    const uint32_t rowaddr = slot + lr * 512;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      uint32_t a[4];
+      ldsm_x4(rowaddr + (((2 * kk + lh) ^ (lr & 7)) << 4), a);
+      MmaT<T>::mma(sc[kk & 1], a, bq[kk][0], bq[kk][1]);
+    }
+    float s0 = (sc[0][0] + sc[1][0]) + (sc[0][1] + sc[1][1]);   // columns of this lane's pair
+    float s1 = (sc[0][2] + sc[1][2]) + (sc[0][3] + sc[1][3]);
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+    s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+    const bool ok0 = ids[j][0] >= 0 && ids[j][0] != pos;
+    const bool ok1 = ids[j][1] >= 0 && ids[j][1] != pos;
+    s0 = ok0 ? s0 / sqrt_d : -INFINITY;                      // row g
+    s1 = ok1 ? s1 / sqrt_d : -INFINITY;                      // row g + 8
+    float tm = fmaxf(s0, s1);
+    tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 4));
+    tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 8));
+    tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 16));
+    if (tm != -INFINITY) {                                   // warp-uniform
+      if (tm > m) {
+        const float corr = expf(m - tm);                     // m == -inf -> 0
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          acc[i][0] *= corr; acc[i][1] *= corr; acc[i][2] *= corr; acc[i][3] *= corr;
+        }
+        l *= corr;
+        m = tm;
+      }
+      const float p0 = expf(s0 - m), p1 = expf(s1 - m);     // exp(-inf) = 0
+      l += p0 + p1;
+      // Pm fragment: rows 2t, 2t+1 (quads 2t, 2t+1) and 2t+8, 2t+9
+      const float pa = __shfl_sync(0xffffffffu, p0, 8 * t);
+      const float pb = __shfl_sync(0xffffffffu, p0, 8 * t + 4);
+      const float pc = __shfl_sync(0xffffffffu, p1, 8 * t);
+      const float pd = __shfl_sync(0xffffffffu, p1, 8 * t + 4);
+      uint32_t pf[4];
+      pf[0] = MmaT<T>::pack(split_part<T>(pa, g), split_part<T>(pb, g));
+      pf[2] = MmaT<T>::pack(split_part<T>(pc, g), split_part<T>(pd, g));
+      if (g >= NS) pf[0] = pf[2] = 0u;
+      pf[1] = pf[3] = 0u;
+#pragma unroll
+      for (int np = 0; np < 8; ++np) {
+        uint32_t v[4];
+        ldsm_x4_t(rowaddr + (((16 + 2 * np + lh) ^ (lr & 7)) << 4), v);
+        MmaT<T>::mma(acc[2 * np], pf, v[0], v[1]);
+        MmaT<T>::mma(acc[2 * np + 1], pf, v[2], v[3]);
+      }
+    }
+    __syncwarp();                                            // slot j % RING free for reuse
+  }
+  if (c == 0 && w == 0) {  // the current token: GPU-resident f32 row, f32 dot
+    const float* qr = q + (size_t)b * ldq + (size_t)h * d;
+    const float* kr = k_cur + (size_t)b * ldkv + (size_t)h * d;
+    float dot = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) dot = fmaf(qr[lane * 4 + i], kr[lane * 4 + i], dot);
+    dot = warp_sum(dot);
+    const float scur = dot / sqrt_d;
+    if (scur > m) {
+      const float corr = expf(m - scur);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        acc[i][0] *= corr; acc[i][1] *= corr; acc[i][2] *= corr; acc[i][3] *= corr;
+      }
+      l *= corr;
+      m = scur;
+    }
+    const float p = expf(scur - m);
+    if (g == 0) {
+      l += p;
+      const float* vr = v_cur + (size_t)b * ldkv + (size_t)h * d;
+#pragma unroll
+      for (int nt = 0; nt < 16; ++nt) {
+        acc[nt][0] = fmaf(p, vr[nt * 8 + 2 * t], acc[nt][0]);
+        acc[nt][1] = fmaf(p, vr[nt * 8 + 2 * t + 1], acc[nt][1]);
+      }
+    }
+  }
+  // O row = sum of the NS split rows; l over the 8 quads
+  l += __shfl_xor_sync(0xffffffffu, l, 4);
+  l += __shfl_xor_sync(0xffffffffu, l, 8);
+  l += __shfl_xor_sync(0xffffffffu, l, 16);
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) {
+      const float x = acc[nt][jj];
+      float y = x + __shfl_down_sync(0xffffffffu, x, 4);
+      if (NS > 2) y += __shfl_down_sync(0xffffffffu, x, 8);
+      if (g == 0) wacc[w][nt * 8 + 2 * t + jj] = y;
+    }
+  }
+  if (lane == 0) { wm[w] = m; wl[w] = l; }
+  __syncthreads();
+  float M = -INFINITY;
+  for (int i = 0; i < kMmaWarps; ++i) M = fmaxf(M, wm[i]);
+  float* part = partial + (bh * max_chunks + c) * (size_t)(d + 2);
+  if (threadIdx.x == 0) {
+    float L = 0.f;
+    for (int i = 0; i < kMmaWarps; ++i) L += wl[i] * (wm[i] == -INFINITY ? 0.f : expf(wm[i] - M));
+    part[0] = M;
+    part[1] = L;
+  }
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    float a = 0.f;
+    for (int i = 0; i < kMmaWarps; ++i) a += wacc[i][e] * (wm[i] == -INFINITY ? 0.f : expf(wm[i] - M));
+    part[2 + e] = a;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(tickets + bh, 1) == nchunks - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const float* pb = partial + bh * max_chunks * (size_t)(d + 2);
+  float MM = -INFINITY;
+  for (int i = 0; i < nchunks; ++i) MM = fmaxf(MM, __ldcg(pb + (size_t)i * (d + 2)));
+  float LL = 0.f;
+  for (int i = 0; i < nchunks; ++i) {
+    const float mi = __ldcg(pb + (size_t)i * (d + 2));
+    LL += __ldcg(pb + (size_t)i * (d + 2) + 1) * (mi == -INFINITY ? 0.f : expf(mi - MM));
+  }
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    float a = 0.f;
+    for (int i = 0; i < nchunks; ++i) {
+      const float mi = __ldcg(pb + (size_t)i * (d + 2));
+      a += __ldcg(pb + (size_t)i * (d + 2) + 2 + e) * (mi == -INFINITY ? 0.f : expf(mi - MM));
+    }
+    out[(size_t)b * ldo + (size_t)h * d + e] = a / LL;
+  }
+  if (threadIdx.x == 0) tickets[bh] = 0;
+}
+
 // IG_ATTEND_IMPL=tma selects the TMA-fed 512-B path.  Measured alone at C3
 // (round 1): register-fed 2.84 TB/s vs TMA-fed 2.39 TB/s -- the per-row math
 // (f16 unpack + shuffle reductions), not the feed, bounds this kernel, so
 // the register-fed loop stays the default.
-inline bool attend_tma_enabled() {
-  static const bool on = [] {
+inline char attend_impl() {   // 'm' (default, tensor cores), 'r' (register-fed), 't' (TMA-fed)
+  static const char impl = [] {
     const char* v = getenv("IG_ATTEND_IMPL");
-    return v && v[0] == 't';
+    return v && (v[0] == 'r' || v[0] == 't') ? v[0] : 'm';
   }();
-  return on;
+  return impl;
 }
+inline bool attend_tma_enabled() { return attend_impl() == 't'; }
 
 template <typename T>
 int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const float* k_cur,
@@ -601,7 +899,19 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
       IG_LAUNCH_STATUS();
       return IG_OK;
     }
-    if (d == 128) {  // 512-B rows, register-fed (default)
+    if (d == 128 && attend_impl() == 'm') {  // 512-B rows on the tensor cores (default)
+      const int mc = (cap + kMmaChunk - 1) / kMmaChunk;
+      constexpr int kRing = 3;
+      const size_t smem = (size_t)kMmaWarps * kRing * kMmaTileBytes;
+      IG_CUDA_STATUS(cudaFuncSetAttribute(attend512_mma_kernel<T, kRing>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attend512_mma_kernel<T, kRing><<<dim3(mc, grid.y, grid.z), kMmaWarps * 32, smem, s>>>(
+          q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, Hg, cap, sqrt_d,
+          max_chunks, partial, tickets, out, ldo);
+      IG_LAUNCH_STATUS();
+      return IG_OK;
+    }
+    if (d == 128) {  // 512-B rows, register-fed (IG_ATTEND_IMPL=r)
       const int mc = (cap + kFastChunk - 1) / kFastChunk;
       attend512_kernel<T><<<dim3(mc, grid.y, grid.z), kAttThreads, 0, s>>>(
           q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, Hg, cap, sqrt_d,

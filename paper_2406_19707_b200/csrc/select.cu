@@ -58,9 +58,15 @@ __device__ __forceinline__ void pick_digit(SelShared& sh, uint32_t prefix, int n
 
 // Top-n rows of a score row, ascending, into out[0:n).  Whole block calls.
 // `keys` is this block's shared buffer of s order keys (filled here).
+// The radix passes stop early once the boundary bin is taken whole (then
+// every key whose resolved digits equal the prefix is selected, no tie rule
+// needed); the compaction gives each warp one contiguous row range, counts it
+// once, and emits with ballots -- two block barriers instead of two per
+// 512-row tile.
 __device__ void radix_topn(const float* __restrict__ row, int s, int n, int32_t* __restrict__ out,
                            SelShared& sh, uint32_t* __restrict__ keys) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int nw = blockDim.x >> 5;
   if (n >= s) {
     for (int t = tid; t < s; t += blockDim.x) out[t] = t;
     return;
@@ -69,7 +75,8 @@ __device__ void radix_topn(const float* __restrict__ row, int s, int n, int32_t*
   for (int t = tid; t < s; t += blockDim.x) keys[t] = order_key(row[t]);
   uint32_t prefix = 0, mask = 0;
   int need = n;
-  for (int pass = 0; pass < 4; ++pass) {
+  bool whole = false;      // boundary bin taken entirely: no tie cut inside it
+  for (int pass = 0; pass < 4 && !whole; ++pass) {
     const int shift = 24 - 8 * pass;
     for (int i = tid; i < 256; i += blockDim.x) sh.hist[i] = 0;
     __syncthreads();
@@ -95,40 +102,40 @@ __device__ void radix_topn(const float* __restrict__ row, int s, int n, int32_t*
     prefix = sh.prefix;
     need = sh.need;
     mask |= 255u << shift;
+    whole = (int)sh.hist[(prefix >> shift) & 255u] == need;
+    __syncthreads();     // hist is rewritten by the next pass
   }
-  const uint32_t pivot = prefix;  // the n-th largest key; take `need` of its ties
+  // take: (key & mask) > prefix, or == prefix and (whole, or among the first
+  // `need` such rows in index order).  Warp w owns rows [w*span, (w+1)*span).
+  const int span = ((s + nw - 1) / nw + 31) & ~31;
+  const int t_lo = min(s, w * span), t_hi = min(s, t_lo + span);
   const unsigned lt_mask = (1u << lane) - 1u;
-  int eq_base = 0, out_base = 0;
-  for (int t0 = 0; t0 < s && out_base < n; t0 += blockDim.x) {
-    const int t = t0 + tid;
-    const uint32_t key = t < s ? keys[t] : 0u;
-    const bool gt = t < s && key > pivot;
-    const bool eq = t < s && key == pivot;
+  int n_gt = 0, n_eq = 0;
+  for (int t0 = t_lo; t0 < t_hi; t0 += 32) {
+    const int t = t0 + lane;
+    const uint32_t km = t < t_hi ? (keys[t] & mask) : 0u;
+    n_gt += __popc(__ballot_sync(0xffffffffu, t < t_hi && km > prefix));
+    n_eq += __popc(__ballot_sync(0xffffffffu, t < t_hi && km == prefix));
+  }
+  if (lane == 0) { sh.warp_a[w] = n_gt; sh.warp_b[w] = n_eq; }
+  __syncthreads();
+  int out_off = 0, eq_before = 0;
+  for (int i = 0; i < w; ++i) {
+    const int e = whole ? sh.warp_b[i] : min(sh.warp_b[i], max(0, need - eq_before));
+    eq_before += sh.warp_b[i];
+    out_off += sh.warp_a[i] + e;
+  }
+  for (int t0 = t_lo; t0 < t_hi; t0 += 32) {
+    const int t = t0 + lane;
+    const uint32_t km = t < t_hi ? (keys[t] & mask) : 0u;
+    const bool gt = t < t_hi && km > prefix;
+    const bool eq = t < t_hi && km == prefix;
     const unsigned eqb = __ballot_sync(0xffffffffu, eq);
-    if (lane == 0) sh.warp_a[w] = __popc(eqb);
-    __syncthreads();
-    int eq_off = eq_base;
-    int eq_tile = 0;
-    for (int i = 0; i < kSelWarps; ++i) {
-      const int c = sh.warp_a[i];
-      if (i < w) eq_off += c;
-      eq_tile += c;
-    }
-    const bool take = gt || (eq && (eq_off + __popc(eqb & lt_mask)) < need);
+    const bool take = gt || (eq && (whole || eq_before + __popc(eqb & lt_mask) < need));
     const unsigned tb = __ballot_sync(0xffffffffu, take);
-    if (lane == 0) sh.warp_b[w] = __popc(tb);
-    __syncthreads();
-    int off = out_base;
-    int tile = 0;
-    for (int i = 0; i < kSelWarps; ++i) {
-      const int c = sh.warp_b[i];
-      if (i < w) off += c;
-      tile += c;
-    }
-    if (take) out[off + __popc(tb & lt_mask)] = t;
-    eq_base += eq_tile;
-    out_base += tile;
-    __syncthreads();
+    if (take) out[out_off + __popc(tb & lt_mask)] = t;
+    out_off += __popc(tb);
+    eq_before += __popc(eqb);
   }
 }
 

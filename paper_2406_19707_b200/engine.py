@@ -781,6 +781,9 @@ class DecodeEngine:
             finally:
                 self._graph_mode = False
             return out
+        if self.x is not self.xbuf[0]:          # replays start from xbuf[0]
+            self.xbuf[0].copy_(self.x)
+            self.x = self.xbuf[0]
         self.compute.wait_stream(cur)
         with torch.cuda.stream(self.compute):
             self._graph.replay()

@@ -259,18 +259,25 @@ def test_sgemm_rows_vs_float64(M, N, K, epilogue, fn):
     assert not tk.any()
 
 
-def test_attend_tma_variant_matches(monkeypatch):
-    """The opt-in TMA-fed attention (IG_ATTEND_IMPL=tma) runs in a subprocess
-    (the switch is read once per process) and must equal the default path."""
+@pytest.mark.parametrize("elt", ["f16", "bf16"])
+def test_attend_512b_row_variants_match(elt):
+    """The three 512-B-row attention kernels -- tensor cores (default), register-fed
+    (IG_ATTEND_IMPL=r), TMA-fed (IG_ATTEND_IMPL=tma) -- each in a subprocess (the
+    switch is read once per process), vs float64 attention over the same rows:
+    ragged row counts, an excluded row (pos), resident slot tables with empty
+    slots (ig_attend_slots)."""
+    import os
     import subprocess
     import sys
+    import tempfile
     code = (
-        "import numpy as np, torch, ctypes\n"
+        "import numpy as np, torch, ctypes, sys\n"
         "from paper_2406_19707_b200 import _lib\n"
         "rng = np.random.default_rng(3)\n"
         "B, Hg, d, cap = 2, 3, 128, 700\n"
         "q = torch.from_numpy(rng.standard_normal((B, 3*Hg*d)).astype(np.float32)).cuda()\n"
-        "stage = torch.from_numpy(rng.standard_normal((B, Hg, cap, 2*d)).astype(np.float16)).cuda()\n"
+        "T = torch.float16 if sys.argv[2] == 'f16' else torch.bfloat16\n"
+        "stage = torch.from_numpy((2*rng.standard_normal((B, Hg, cap, 2*d))).astype(np.float32)).to(T).cuda()\n"
         "n = torch.tensor([700, 37], dtype=torch.int32, device='cuda')\n"
         "idx = torch.from_numpy(np.tile(np.arange(cap, dtype=np.int32), (B, Hg, 1))).cuda()\n"
         "pos = torch.full((B, Hg), 5, dtype=torch.int32, device='cuda')\n"
@@ -280,20 +287,46 @@ def test_attend_tma_variant_matches(monkeypatch):
         "part = torch.empty(pf.value, device='cuda'); tick = torch.zeros(tk.value, dtype=torch.int32, device='cuda')\n"
         "out = torch.empty((B, Hg*d), device='cuda')\n"
         "_lib.call('ig_attend', q.data_ptr(), 3*Hg*d, q.data_ptr()+4*Hg*d, q.data_ptr()+8*Hg*d, 3*Hg*d, stage.data_ptr(),"
-        " _lib.ELT['f16'], idx.data_ptr(), n.data_ptr(), pos.data_ptr(), st.data_ptr(), B, Hg, d, cap, part.data_ptr(),"
+        " _lib.ELT[sys.argv[2]], idx.data_ptr(), n.data_ptr(), pos.data_ptr(), st.data_ptr(), B, Hg, d, cap, part.data_ptr(),"
         " tick.data_ptr(), out.data_ptr(), Hg*d, _lib.stream_handle())\n"
-        "np.save(__import__('sys').argv[1], out.cpu().numpy())\n")
-    import os
-    import tempfile
-    outs = []
-    for impl in ("ldg", "tma"):
-        f = os.path.join(tempfile.mkdtemp(), "o.npy")
+        "slot = idx.clone(); slot[:, :, 1::7] = -1\n"
+        "used = torch.tensor([[700, 650, 9], [1, 0, 300]], dtype=torch.int32, device='cuda')\n"
+        "out2 = torch.empty((B, Hg*d), device='cuda')\n"
+        "_lib.call('ig_attend_slots', q.data_ptr(), 3*Hg*d, q.data_ptr()+4*Hg*d, q.data_ptr()+8*Hg*d, 3*Hg*d,"
+        " stage.data_ptr(), _lib.ELT[sys.argv[2]], slot.data_ptr(), used.data_ptr(), pos.data_ptr(), st.data_ptr(),"
+        " B, Hg, d, cap, part.data_ptr(), tick.data_ptr(), out2.data_ptr(), Hg*d, _lib.stream_handle())\n"
+        "np.savez(sys.argv[1], out=out.cpu().numpy(), out2=out2.cpu().numpy(), q=q.cpu().numpy(),"
+        " stage=stage.float().cpu().numpy(), slot=slot.cpu().numpy(), used=used.cpu().numpy())\n")
+    res = {}
+    for impl in ("mma", "r", "tma"):
+        f = os.path.join(tempfile.mkdtemp(), "o.npz")
         env = dict(os.environ, IG_ATTEND_IMPL=impl)
-        r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True,
+        r = subprocess.run([sys.executable, "-c", code, f, elt], env=env, capture_output=True, text=True,
                            cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         assert r.returncode == 0, r.stderr[-2000:]
-        outs.append(np.load(f))
-    np.testing.assert_allclose(outs[0], outs[1], rtol=1e-5, atol=1e-6)
+        res[impl] = np.load(f)
+    z = res["mma"]
+    qn, stg = z["q"].astype(np.float64), z["stage"].astype(np.float64)
+    B, Hg, d = 2, 3, 128
+
+    def ref(b, h, rows):
+        K = np.concatenate([stg[b, h, rows, :d], qn[b, Hg * d + h * d:Hg * d + (h + 1) * d][None]])
+        V = np.concatenate([stg[b, h, rows, d:], qn[b, 2 * Hg * d + h * d:2 * Hg * d + (h + 1) * d][None]])
+        lg = K @ qn[b, h * d:(h + 1) * d] / np.sqrt(d)
+        w = np.exp(lg - lg.max())
+        return (w / w.sum()) @ V
+
+    for impl, o in res.items():
+        for b, nb in enumerate((700, 37)):
+            for h in range(Hg):
+                exp = ref(b, h, [i for i in range(nb) if i != 5])
+                np.testing.assert_allclose(o["out"][b, h * d:(h + 1) * d], exp, rtol=2e-5, atol=2e-5,
+                                           err_msg=impl)
+                used = int(z["used"][b, h])
+                rows = [i for i in range(used) if z["slot"][b, h, i] >= 0 and z["slot"][b, h, i] != 5]
+                exp2 = ref(b, h, rows)
+                np.testing.assert_allclose(o["out2"][b, h * d:(h + 1) * d], exp2, rtol=2e-5, atol=2e-5,
+                                           err_msg=impl + " slots")
 
 
 def test_shim_error_paths_match_reference():

@@ -239,3 +239,28 @@ def test_resident_rejects_bad_combinations():
         DecodeEngine(plain, engine_cfg(run_config("full")), resident=True)
     with pytest.raises(ValueError):
         DecodeEngine(sk, engine_cfg(run_config("spec")), resident=True, hbm_layers=1)
+
+
+def test_graph_replay_interleaved_with_eager_steps():
+    """bench.py replays the captured step, then runs eager (instrumented) steps,
+    then replays again: with an odd layer count the eager steps leave x in the
+    second buffer, and the replays must still continue from it."""
+    from paper_2406_19707_b200 import DecodeEngine
+    _, sk = models("m256")                      # 3 layers
+    ocfg = run_config("spec", gen_len=9)
+    sessions = oracle_sessions(sk, ocfg)
+    outs = []
+    for mode in ("eager", "mixed"):
+        eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg, record_selection=False),
+                                         copy.deepcopy(sessions), pool_dtype="f16", resident=True,
+                                         cuda_graph=(mode == "mixed"))
+        try:
+            o = []
+            for i in range(ocfg.gen_len):
+                if mode == "mixed":
+                    eng.cuda_graph = i not in (3, 4, 6)
+                o.append(eng.decode_step().cpu().numpy())
+            outs.append(np.stack(o))
+        finally:
+            eng.close()
+    np.testing.assert_array_equal(outs[0], outs[1])
