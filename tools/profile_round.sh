@@ -4,5 +4,5 @@
 R=${1:-r01}
 mkdir -p gpurun_out
 IG_PROFILE_WINDOW=1 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file gpurun_out/launches_${R}.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-hbm-variant \
+    --log-file gpurun_out/launches_${R}.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-variant \
     > gpurun_out/launches_${R}.bench.json 2> gpurun_out/launches_${R}.err
