@@ -247,7 +247,11 @@ __device__ __forceinline__ void mma_tf32(float* c, const uint32_t* a, uint32_t b
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-template <int MTILES, int STAGES>   // 16-row M tiles (M <= 16 * MTILES), pipeline depth
+// KIN = 2: the 8 warps form 2 groups over the k8 steps of each stage (warp
+// w: columns 32 (w & 3) .. +31, k8 steps 2 (w >> 2), +1) and the groups'
+// accumulators are summed through shared memory at the end (fixed order);
+// KIN = 1: warp w owns columns 16 w .. +15 over all k8 steps.
+template <int MTILES, int STAGES, int KIN>   // 16-row M tiles (M <= 16 * MTILES), pipeline depth
 __global__ void __launch_bounds__(kGemmWarps * 32, (MTILES == 1 ? (STAGES <= 3 ? 3 : 2) : 1))
 sgemm_tc_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ W, int ldw,
                 float* __restrict__ Y, int ldy, const float* __restrict__ R, int ldr, int M, int N,
@@ -271,11 +275,12 @@ sgemm_tc_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ 
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   auto load_stage = [&](int c, int st) { ld.load(c, sbase + st * kStage * 4, kTcWPitch); };
 
-  float big[MTILES][2][4], small[MTILES][2][4], small2[MTILES][2][4];
+  constexpr int NT = 2 * KIN;                  // n8 tiles per warp
+  float big[MTILES][NT][4], small[MTILES][NT][4], small2[MTILES][NT][4];
 #pragma unroll
   for (int mt = 0; mt < MTILES; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int i = 0; i < 4; ++i) big[mt][nt][i] = small[mt][nt][i] = small2[mt][nt][i] = 0.f;
 
@@ -284,7 +289,8 @@ sgemm_tc_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ 
     if (i < nch) load_stage(i, i);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  const int wn = w * 16;                       // my 16 columns of the tile
+  const int wn = KIN == 2 ? (w & 3) * 32 : w * 16;   // my columns of the tile
+  const int k8lo = KIN == 2 ? (w >> 2) * 16 : 0;      // my k8 steps of each stage
   for (int c = 0; c < nch; ++c) {
     const int st = c % STAGES;
     asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 2) : "memory");
@@ -295,7 +301,8 @@ sgemm_tc_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ 
     const float* ws_ = smem + st * kStage;
     const float* xs_ = ws_ + kWs;
 #pragma unroll
-    for (int k8 = 0; k8 < kGemmKT; k8 += 8) {
+    for (int kq = 0; kq < kGemmKT / KIN; kq += 8) {
+      const int k8 = k8lo + kq;
       uint32_t ahi[MTILES][4], alo[MTILES][4];
 #pragma unroll
       for (int mt = 0; mt < MTILES; ++mt) {
@@ -306,7 +313,7 @@ sgemm_tc_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ 
         split_tf32(xr[8 * kTcXPitch + 4], ahi[mt][3], alo[mt][3]);
       }
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
+      for (int nt = 0; nt < NT; ++nt) {
         const float* wr = ws_ + (k8 + t) * kTcWPitch + wn + nt * 8 + g;
         uint32_t bhi0, blo0, bhi1, blo1;
         split_tf32(wr[0], bhi0, blo0);
@@ -321,22 +328,51 @@ sgemm_tc_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ 
     }
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+  for (int mt = 0; mt < MTILES; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) big[mt][nt][i] += small[mt][nt][i] + small2[mt][nt][i];
+  if (KIN == 2) {              // k-group 1 hands its sums to k-group 0 through shared memory
+    __syncthreads();           // every warp is past its last stage read
+    float* red = smem;         // [4 warps][MTILES][NT][4][32 lanes]
+    constexpr int per = MTILES * NT * 4;
+    if (w >= 4) {
+#pragma unroll
+      for (int mt = 0; mt < MTILES; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            red[(((w - 4) * per) + (mt * NT + nt) * 4 + i) * 32 + lane] = big[mt][nt][i];
+    }
+    __syncthreads();
+    if (w < 4) {
+#pragma unroll
+      for (int mt = 0; mt < MTILES; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            big[mt][nt][i] += red[((w * per) + (mt * NT + nt) * 4 + i) * 32 + lane];
+    }
+  }
   const size_t tile_elems = (size_t)M * kGemmTileN;
   float* part = ws + ((size_t)tile * ksplit + ks) * tile_elems;
 #pragma unroll
   for (int mt = 0; mt < MTILES; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
+    for (int nt = 0; nt < NT; ++nt) {
+      if (KIN == 2 && w >= 4) break;
       const int col = wn + nt * 8 + 2 * t;
       const int r0 = mt * 16 + g, r1 = r0 + 8;
       if (r0 < M)
         *reinterpret_cast<float2*>(part + (size_t)r0 * kGemmTileN + col) =
-            make_float2(big[mt][nt][0] + (small[mt][nt][0] + small2[mt][nt][0]),
-                        big[mt][nt][1] + (small[mt][nt][1] + small2[mt][nt][1]));
+            make_float2(big[mt][nt][0], big[mt][nt][1]);
       if (r1 < M)
         *reinterpret_cast<float2*>(part + (size_t)r1 * kGemmTileN + col) =
-            make_float2(big[mt][nt][2] + (small[mt][nt][2] + small2[mt][nt][2]),
-                        big[mt][nt][3] + (small[mt][nt][3] + small2[mt][nt][3]));
+            make_float2(big[mt][nt][2], big[mt][nt][3]);
     }
   if (ksplit == 1) {
     __syncthreads();
@@ -361,16 +397,16 @@ sgemm_tc_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ 
   if (tid == 0 && ksplit > 1) tickets[tile] = 0;
 }
 
-template <int MTILES, int STAGES>
+template <int MTILES, int STAGES, int KIN>
 int launch_sgemm_tc(const float* X, int ldx, const float* W, int ldw, float* Y, int ldy,
                     const float* R, int ldr, int M, int N, int K, int ksplit, int epilogue,
                     float* ws, int32_t* tickets, cudaStream_t s) {
   const int tiles = (N + kGemmTileN - 1) / kGemmTileN;
   const size_t smem =
       (size_t)STAGES * (kGemmKT * kTcWPitch + 16 * MTILES * kTcXPitch) * sizeof(float);
-  IG_CUDA_STATUS(cudaFuncSetAttribute(sgemm_tc_kernel<MTILES, STAGES>,
+  IG_CUDA_STATUS(cudaFuncSetAttribute(sgemm_tc_kernel<MTILES, STAGES, KIN>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  sgemm_tc_kernel<MTILES, STAGES><<<dim3(tiles, ksplit), kGemmWarps * 32, smem, s>>>(
+  sgemm_tc_kernel<MTILES, STAGES, KIN><<<dim3(tiles, ksplit), kGemmWarps * 32, smem, s>>>(
       X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, ws, tickets);
   IG_LAUNCH_STATUS();
   return IG_OK;
@@ -426,13 +462,14 @@ extern "C" int ig_sgemm_rows(const float* X, int ldx, const float* W, int ldw, f
 extern "C" int ig_sgemm_tc_ksplit(int M, int N, int K) {
   // Measured (tools/gemm_probe.py --ksplit all, C3 shapes, profiles/r01b_gemm_probe.jsonl):
   // ~1900 CTAs (>= 4 waves of 3 CTAs/SM) beat the wave-filling rule of
-  // ig_sgemm_rows_ksplit by 5-15%; more than 16 splits only adds merge traffic.
+  // ig_sgemm_rows_ksplit by 5-15%, as long as each CTA keeps >= 10 chunks
+  // (profiles/r01e_gemm_variants.md).
   (void)M;
   const int tiles = (N + ig::kGemmTileN - 1) / ig::kGemmTileN;
   const int chunks = (K + ig::kGemmKT - 1) / ig::kGemmKT;
   int ks = (1920 + tiles - 1) / tiles;
-  if (ks > 16) ks = 16;
-  if (ks > chunks / 4) ks = chunks / 4;
+  if (ks > 32) ks = 32;
+  if (ks > chunks / 10) ks = chunks / 10;     // >= 10 pipeline chunks per CTA
   return ks < 1 ? 1 : ks;
 }
 
@@ -449,14 +486,18 @@ extern "C" int ig_sgemm_tc(const float* X, int ldx, const float* W, int ldw, flo
   const int tiles = (N + kGemmTileN - 1) / kGemmTileN;
   if ((size_t)tiles * ksplit * M * kGemmTileN > workspace_floats) return IG_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
-  static const int stages = [] {
-    const char* v = getenv("IG_TC_STAGES");   // tuning sweeps only
-    return v ? atoi(v) : 3;
+  static const int variant = [] {
+    // tuning sweeps only (profiles/r01e_gemm_variants.md): 1 = (3 stages, KIN 2, default),
+    // 0 = (3 stages, KIN 1), 2 = (4 stages, KIN 1)
+    const char* v = getenv("IG_TC_VARIANT");
+    return v ? atoi(v) : 1;
   }();
   if (M <= 16) {
-    if (stages == 4)
-      return launch_sgemm_tc<1, 4>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
-    return launch_sgemm_tc<1, 3>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
+    if (variant == 0)
+      return launch_sgemm_tc<1, 3, 1>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
+    if (variant == 2)
+      return launch_sgemm_tc<1, 4, 1>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
+    return launch_sgemm_tc<1, 3, 2>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
   }
-  return launch_sgemm_tc<2, 4>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
+  return launch_sgemm_tc<2, 4, 1>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
 }

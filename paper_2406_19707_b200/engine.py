@@ -246,9 +246,21 @@ class DecodeEngine:
         dev, d, Hg, h0 = self.device, self.d, self.Hg, self.h0
         c0, c1 = h0 * d, (h0 + Hg) * d
         self.wqkv, self.wo, self.ffn_in, self.ffn_out, self.ln = [], [], [], [], []
-        for lw in model.layers:
+        # wfused[li] = [W_Q | W_K | W_V](li) | W_Q(li+1) over this rank's heads: the
+        # projections of layer li and the speculation query of layer li+1 read the
+        # same input x_a(li) (engine.py:311-327 / speculation.py:133), so one
+        # GEMM launch streams both (W_Q(li+1) is stored twice); wqkv[li] is a view.
+        self.wfused = []
+        layers = list(model.layers)
+        spec_ = getattr(self.config.scheme, "value", self.config.scheme) == "speculative"
+        for li, lw in enumerate(layers):
             q, k, v = (_f32(getattr(lw, f), dev) for f in ("w_q", "w_k", "w_v"))
-            self.wqkv.append(torch.cat([q[:, c0:c1], k[:, c0:c1], v[:, c0:c1]], dim=1).contiguous())
+            parts = [q[:, c0:c1], k[:, c0:c1], v[:, c0:c1]]
+            if spec_ and li + 1 < len(layers):
+                parts.append(_f32(layers[li + 1].w_q, dev)[:, c0:c1])
+            wf = torch.cat(parts, dim=1).contiguous()
+            self.wfused.append(wf if len(parts) == 4 else None)
+            self.wqkv.append(wf[:, :3 * (c1 - c0)])
             self.wo.append(_f32(lw.w_o, dev)[c0:c1].contiguous())
             self.ffn_in.append(_f32(lw.ffn_in, dev))
             self.ffn_out.append(_f32(lw.ffn_out, dev))
@@ -275,8 +287,10 @@ class DecodeEngine:
         self.x = self.xbuf[0]
         self.x_a = torch.empty((B, D), dtype=f32, device=dev)
         self.x_f = torch.empty((B, D), dtype=f32, device=dev)
-        self.qspec = torch.empty((B, Hg * d), dtype=f32, device=dev)
-        self.qkv = torch.empty((B, 3 * Hg * d), dtype=f32, device=dev)
+        # [q | k | v | qspec(next layer)] per sequence, one row of the fused GEMM
+        self.qkvq = torch.empty((B, 4 * Hg * d), dtype=f32, device=dev)
+        self.qkv = self.qkvq[:, :3 * Hg * d]
+        self.qspec = self.qkvq[:, 3 * Hg * d:]
         self.attn = torch.empty((B, Hg * d), dtype=f32, device=dev)
         self.o = torch.empty((B, D), dtype=f32, device=dev)
         self.hidden = torch.empty((B, F), dtype=f32, device=dev)
@@ -655,7 +669,7 @@ class DecodeEngine:
 
         def rehearse():
             self.count_sum[li].zero_()
-            _lib.call("ig_rehearse_count", self.qspec.data_ptr(), Hgd, self.cols[li].data_ptr(),
+            _lib.call("ig_rehearse_count", self.qspec.data_ptr(), self.qkvq.stride(0), self.cols[li].data_ptr(),
                       self.pk[li - 1].data_ptr(), self.st.data_ptr(), B, Hg, d, kc, S, self.scale,
                       float(sc.alpha), self.scores.data_ptr(), self.maxkey.data_ptr(),
                       self.rtickets.data_ptr(), self.counts.data_ptr(),
@@ -701,12 +715,10 @@ class DecodeEngine:
         M, K = X.shape
         N = W.shape[1]
         if self.dense == "cublas":
-            if epilogue == 2:
-                torch.addmm(R, X, W, out=Y)
-            else:
-                torch.matmul(X, W, out=Y)
-                if epilogue == 1:
-                    Y.relu_()
+            res = torch.addmm(R, X, W) if epilogue == 2 else torch.matmul(X, W)
+            if epilogue == 1:
+                res.relu_()
+            Y.copy_(res)              # Y may be a strided view (qkv of the fused buffer)
             return
         ksp = self.gemm_ksplit.get((N, K)) or self._ksplit(M, N, K)
         if self._inst is not None:
@@ -734,18 +746,18 @@ class DecodeEngine:
 
     def _attend(self, li: int, stage, idx, n, stage_rows: int, cs: int) -> None:
         Hgd = self.Hg * self.d
-        q = self.qkv
-        _lib.call("ig_attend", q.data_ptr(), 3 * Hgd, q.data_ptr() + 4 * Hgd,
-                  q.data_ptr() + 8 * Hgd, 3 * Hgd, stage.data_ptr(), _lib.ELT[self.elt],
+        q, ld = self.qkv, self.qkvq.stride(0)
+        _lib.call("ig_attend", q.data_ptr(), ld, q.data_ptr() + 4 * Hgd,
+                  q.data_ptr() + 8 * Hgd, ld, stage.data_ptr(), _lib.ELT[self.elt],
                   _lib.ptr(idx), _lib.ptr(n), self.pos[li].data_ptr(), self.st.data_ptr(),
                   self.B, self.Hg, self.d, stage_rows, self.att_partial.data_ptr(),
                   self.att_tickets.data_ptr(), self.attn.data_ptr(), Hgd, cs)
 
     def _attend_slots(self, li: int, cs: int) -> None:
         Hgd = self.Hg * self.d
-        q = self.qkv
-        _lib.call("ig_attend_slots", q.data_ptr(), 3 * Hgd, q.data_ptr() + 4 * Hgd,
-                  q.data_ptr() + 8 * Hgd, 3 * Hgd, self.stage_res[li - 1].data_ptr(),
+        q, ld = self.qkv, self.qkvq.stride(0)
+        _lib.call("ig_attend_slots", q.data_ptr(), ld, q.data_ptr() + 4 * Hgd,
+                  q.data_ptr() + 8 * Hgd, ld, self.stage_res[li - 1].data_ptr(),
                   _lib.ELT[self.elt], self.slot_id[li - 1].data_ptr(),
                   self.slot_used[li - 1].data_ptr(), self.pos[li].data_ptr(), self.st.data_ptr(),
                   self.B, self.Hg, self.d, self.cap, self.att_partial.data_ptr(),
@@ -840,9 +852,10 @@ class DecodeEngine:
                 nxt = li + 1
                 if nxt < L:
                     if speculative:
-                        self._gemm(self.x_a, self.wqkv[nxt][:, :Hgd], self.qspec, cs)
+                        # q/k/v of this layer + the speculation query of the next
+                        self._gemm(self.x_a, self.wfused[li], self.qkvq, cs)
                         self._mark("rehearse", nxt, C, True)
-                        _lib.call("ig_rehearse_count", self.qspec.data_ptr(), Hgd,
+                        _lib.call("ig_rehearse_count", self.qspec.data_ptr(), self.qkvq.stride(0),
                                   self.cols[nxt].data_ptr(), self.pk[nxt - 1].data_ptr(),
                                   self.st.data_ptr(), B, Hg, d, self.kcols, self.S_max,
                                   self.scale, float(sc.alpha), self.scores.data_ptr(),
@@ -901,10 +914,12 @@ class DecodeEngine:
                         else:
                             self._issue_full_fetch(nxt, s, self.stage_full[nxt % 2])
                     self.ev_fetch[nxt].record(Fs)
-                self._gemm(self.x_a, self.wqkv[li], self.qkv, cs)
+                if not (speculative and nxt < L):      # else computed by the fused GEMM
+                    self._gemm(self.x_a, self.wqkv[li], self.qkv, cs)
                 sel = speculative and li >= 1
+                ldq = self.qkvq.stride(0)
                 _lib.call("ig_append", self.qkv.data_ptr() + 4 * Hgd, self.qkv.data_ptr() + 8 * Hgd,
-                          3 * Hgd, self._pool_layer_dev(li), _lib.ELT[self.elt],
+                          ldq, self._pool_layer_dev(li), _lib.ELT[self.elt],
                           _lib.ptr(self.pk[li - 1]) if sel else None,
                           _lib.ptr(self.cols[li]) if sel else None, self.kcols,
                           self.arrival[li].data_ptr(), self.lastf[li].data_ptr(),
@@ -915,7 +930,7 @@ class DecodeEngine:
                           self.events[li].data_ptr(), cs)
                 if resident and li == 0:            # keep layer 0's mirror complete
                     _lib.call("ig_stage_put", self.qkv.data_ptr() + 4 * Hgd,
-                              self.qkv.data_ptr() + 8 * Hgd, 3 * Hgd, self.pos[0].data_ptr(),
+                              self.qkv.data_ptr() + 8 * Hgd, ldq, self.pos[0].data_ptr(),
                               self.stage_full[0].data_ptr(), _lib.ELT[self.elt], B, Hg, d,
                               self.S_max, cs)
                 C.wait_event(self.ev_fetch[li])
