@@ -580,8 +580,10 @@ attend512_tma_kernel(const float* __restrict__ q, int ldq, const float* __restri
 //           0..NS-1 = the f32 query split into NS parts exactly representable
 //           in T (q = q0 + q1 (+ q2)), so S[r][0] + .. + S[r][NS-1] is q.k to
 //           ~2^-22 (f16: NS = 2, bf16: NS = 3);
-//   output  O[16 x 128] += Pm[16 x 16 rows] . V_tile[16 x 128], Pm's rows
-//           0..NS-1 = the split softmax weights p of the tile's 16 rows.
+//   output  O^T[128 x 8] += V_tile^T[128 x 16 rows] . Pm[16 rows x 8], Pm's
+//           columns 0..NS-1 = the split softmax weights p of the tile's rows
+//           (d on the MMA's M side: 8 MMAs and 32 accumulator registers per
+//           tile instead of 16 / 64 with p on the M side).
 // f32 accumulation throughout; scores are (q.k) / float32(sqrt(d)) as in
 // model.py:174 and exp is expf.  Rows stream into a per-warp shared-memory
 // ring by cp.async (16-B chunk c of row r stored at chunk c ^ (r & 7), so the
@@ -590,8 +592,7 @@ attend512_tma_kernel(const float* __restrict__ q, int ldq, const float* __restri
 // fixed order as in attend512_kernel (deterministic).
 // ---------------------------------------------------------------------------
 constexpr int kMmaWarps = 4;
-constexpr int kMmaTPW = 8;                                  // tiles per warp
-constexpr int kMmaChunk = kMmaWarps * kMmaTPW * 16;          // 512 rows per CTA
+constexpr int kMmaTPW = 8;                                  // tiles per warp (default)
 constexpr int kMmaTileBytes = 16 * 512;
 
 template <typename T> struct MmaT;
@@ -647,8 +648,8 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t* r) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
 }
 
-template <typename T, int RING>
-__global__ void __launch_bounds__(kMmaWarps * 32, 2)
+template <typename T, int RING, int TPW>
+__global__ void __launch_bounds__(kMmaWarps * 32, RING <= 2 ? 3 : 2)
 attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_cur,
                      const float* __restrict__ v_cur, int ldkv, const T* __restrict__ stage,
                      const int32_t* __restrict__ idx, const int32_t* __restrict__ n_in,
@@ -664,12 +665,14 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
   const int b = blockIdx.z, h = blockIdx.y, c = blockIdx.x;
   const size_t bh = (size_t)b * Hg + h;
   const int rows = att_rows(rows_bh, n_in, st, b, bh);
-  const int nchunks = max(1, (rows + kMmaChunk - 1) / kMmaChunk);
+  const int nchunks = max(1, (rows + (kMmaWarps * TPW * 16) - 1) / (kMmaWarps * TPW * 16));
   if (c >= nchunks) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int pos = pos_in[bh];
-  const int r0 = c * kMmaChunk, r1 = min(rows, r0 + kMmaChunk);
+  // balanced chunks: nchunks of at most warps*TPW*16 rows, sizes within one 64-row tile group
+  const int crows = (((rows + nchunks - 1) / nchunks) + 63) & ~63;
+  const int r0 = c * crows, r1 = min(rows, r0 + crows);
   const uint8_t* src = reinterpret_cast<const uint8_t*>(stage + bh * (size_t)cap * 2 * d);
   const uint32_t ring = (uint32_t)__cvta_generic_to_shared(att_ring) + w * RING * kMmaTileBytes;
 
@@ -686,12 +689,12 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
     }
   }
   float m = -INFINITY, l = 0.f;
-  float acc[16][4];
+  float acc[8][4];                 // [m-tile of d][C fragment]: (d, split col) pairs
 #pragma unroll
-  for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
 
   // tile j of this warp: rows [tb, tb + 16), tb = r0 + (j * warps + w) * 16
-  int ids[kMmaTPW][2];
+  int ids[TPW][2];
   auto issue = [&](int j) {
     const int tb = r0 + (j * kMmaWarps + w) * 16;
     const uint32_t slot = ring + (j % RING) * kMmaTileBytes;
@@ -713,13 +716,13 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
   };
   int ntiles = 0;
 #pragma unroll
-  for (int j = 0; j < kMmaTPW; ++j) ntiles += (r0 + (j * kMmaWarps + w) * 16 < r1) ? 1 : 0;
+  for (int j = 0; j < TPW; ++j) ntiles += (r0 + (j * kMmaWarps + w) * 16 < r1) ? 1 : 0;
 
 #pragma unroll
   for (int j = 0; j < RING - 1; ++j)
     if (j < ntiles) issue(j);
 #pragma unroll
-  for (int j = 0; j < kMmaTPW; ++j) {
+  for (int j = 0; j < TPW; ++j) {
     if (j >= ntiles) break;
     if (j + RING - 1 < ntiles) {
       issue(j + RING - 1);
@@ -757,7 +760,7 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
       if (tm > m) {
         const float corr = expf(m - tm);                     // m == -inf -> 0
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int i = 0; i < 8; ++i) {
           acc[i][0] *= corr; acc[i][1] *= corr; acc[i][2] *= corr; acc[i][3] *= corr;
         }
         l *= corr;
@@ -770,17 +773,20 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
       const float pb = __shfl_sync(0xffffffffu, p0, 8 * t + 4);
       const float pc = __shfl_sync(0xffffffffu, p1, 8 * t);
       const float pd = __shfl_sync(0xffffffffu, p1, 8 * t + 4);
-      uint32_t pf[4];
-      pf[0] = MmaT<T>::pack(split_part<T>(pa, g), split_part<T>(pb, g));
-      pf[2] = MmaT<T>::pack(split_part<T>(pc, g), split_part<T>(pd, g));
-      if (g >= NS) pf[0] = pf[2] = 0u;
-      pf[1] = pf[3] = 0u;
+      // B = Pm: k = tile rows 2t, 2t+1 (b0) and 2t+8, 2t+9 (b1), column g
+      uint32_t pb0 = MmaT<T>::pack(split_part<T>(pa, g), split_part<T>(pb, g));
+      uint32_t pb1 = MmaT<T>::pack(split_part<T>(pc, g), split_part<T>(pd, g));
+      if (g >= NS) pb0 = pb1 = 0u;
+      // A = V^T (m = d, k = row): ldmatrix.trans of the blocks (rows 0-7 | 8-15) x
+      // (d 0-7 | 8-15) of m-tile mt; lane -> row (lane & 7) + 8 (lane >> 4),
+      // chunk 16 + 2 mt + ((lane >> 3) & 1)
+      const int vr = (lane & 7) + ((lane >> 4) << 3), vc = (lane >> 3) & 1;
+      const uint32_t vaddr = slot + vr * 512;
 #pragma unroll
-      for (int np = 0; np < 8; ++np) {
-        uint32_t v[4];
-        ldsm_x4_t(rowaddr + (((16 + 2 * np + lh) ^ (lr & 7)) << 4), v);
-        MmaT<T>::mma(acc[2 * np], pf, v[0], v[1]);
-        MmaT<T>::mma(acc[2 * np + 1], pf, v[2], v[3]);
+      for (int mt = 0; mt < 8; ++mt) {
+        uint32_t a[4];
+        ldsm_x4_t(vaddr + (((16 + 2 * mt + vc) ^ (vr & 7)) << 4), a);
+        MmaT<T>::mma(acc[mt], a, pb0, pb1);
       }
     }
     __syncwarp();                                            // slot j % RING free for reuse
@@ -803,13 +809,13 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
       m = scur;
     }
     const float p = expf(scur - m);
-    if (g == 0) {
-      l += p;
-      const float* vr = v_cur + (size_t)b * ldkv + (size_t)h * d;
+    if (g == 0) l += p;
+    if (t == 0) {                  // split column 0 of rows d = 16 mt + g (+ 8)
+      const float* vrow = v_cur + (size_t)b * ldkv + (size_t)h * d;
 #pragma unroll
-      for (int nt = 0; nt < 16; ++nt) {
-        acc[nt][0] = fmaf(p, vr[nt * 8 + 2 * t], acc[nt][0]);
-        acc[nt][1] = fmaf(p, vr[nt * 8 + 2 * t + 1], acc[nt][1]);
+      for (int mt = 0; mt < 8; ++mt) {
+        acc[mt][0] = fmaf(p, vrow[mt * 16 + g], acc[mt][0]);
+        acc[mt][2] = fmaf(p, vrow[mt * 16 + g + 8], acc[mt][2]);
       }
     }
   }
@@ -818,13 +824,15 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
   l += __shfl_xor_sync(0xffffffffu, l, 8);
   l += __shfl_xor_sync(0xffffffffu, l, 16);
 #pragma unroll
-  for (int nt = 0; nt < 16; ++nt) {
-#pragma unroll
-    for (int jj = 0; jj < 2; ++jj) {
-      const float x = acc[nt][jj];
-      float y = x + __shfl_down_sync(0xffffffffu, x, 4);
-      if (NS > 2) y += __shfl_down_sync(0xffffffffu, x, 8);
-      if (g == 0) wacc[w][nt * 8 + 2 * t + jj] = y;
+  for (int mt = 0; mt < 8; ++mt) {        // sum the split columns (lanes t = 0..3)
+    float y0 = acc[mt][0] + acc[mt][1], y1 = acc[mt][2] + acc[mt][3];
+    y0 += __shfl_xor_sync(0xffffffffu, y0, 1);
+    y1 += __shfl_xor_sync(0xffffffffu, y1, 1);
+    y0 += __shfl_xor_sync(0xffffffffu, y0, 2);
+    y1 += __shfl_xor_sync(0xffffffffu, y1, 2);
+    if (t == 0) {
+      wacc[w][mt * 16 + g] = y0;
+      wacc[w][mt * 16 + g + 8] = y1;
     }
   }
   if (lane == 0) { wm[w] = m; wl[w] = l; }
@@ -900,14 +908,30 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
       return IG_OK;
     }
     if (d == 128 && attend_impl() == 'm') {  // 512-B rows on the tensor cores (default)
-      const int mc = (cap + kMmaChunk - 1) / kMmaChunk;
-      constexpr int kRing = 3;
-      const size_t smem = (size_t)kMmaWarps * kRing * kMmaTileBytes;
-      IG_CUDA_STATUS(cudaFuncSetAttribute(attend512_mma_kernel<T, kRing>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attend512_mma_kernel<T, kRing><<<dim3(mc, grid.y, grid.z), kMmaWarps * 32, smem, s>>>(
-          q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, Hg, cap, sqrt_d,
-          max_chunks, partial, tickets, out, ldo);
+      // tuning sweeps only (IG_ATT_VARIANT): 0 = ring 2 x 8 tiles/warp (3 CTAs/SM, default),
+      // 1 = ring 2 x 4 tiles, 2 = ring 3 x 8 tiles (2 CTAs/SM), 3 = ring 2 x 16 tiles
+      static const int variant = [] {
+        const char* v = getenv("IG_ATT_VARIANT");
+        return v ? atoi(v) : 0;
+      }();
+#define IG_ATT_MMA(RING, TPW)                                                                  \
+  do {                                                                                         \
+    const int chunk = kMmaWarps * (TPW) * 16;                                                  \
+    const dim3 g3((cap + chunk - 1) / chunk, grid.y, grid.z);                                  \
+    const size_t smem = (size_t)kMmaWarps * (RING) * kMmaTileBytes;                            \
+    IG_CUDA_STATUS(cudaFuncSetAttribute(attend512_mma_kernel<T, RING, TPW>,                    \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    attend512_mma_kernel<T, RING, TPW><<<g3, kMmaWarps * 32, smem, s>>>(                       \
+        q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, Hg, cap, sqrt_d, \
+        max_chunks, partial, tickets, out, ldo);                                               \
+  } while (0)
+      switch (variant) {
+        case 1: IG_ATT_MMA(2, 4); break;
+        case 2: IG_ATT_MMA(3, 8); break;
+        case 3: IG_ATT_MMA(2, 16); break;
+        default: IG_ATT_MMA(2, 8); break;
+      }
+#undef IG_ATT_MMA
       IG_LAUNCH_STATUS();
       return IG_OK;
     }
