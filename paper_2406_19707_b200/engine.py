@@ -166,13 +166,17 @@ class DecodeEngine:
         The host pool stays authoritative (every append still goes to it) and
         the attended rows, selections and traces are those of the default path
         (csrc/resident.cu).
+    spec_stream : run layer l+1's speculation chain (rehearse -> [count all-reduce]
+        -> select -> resident plan) on its own high-priority stream, overlapping
+        layer l's append/attention/W_O/FFN (traces recorded with scores use the
+        compute stream).
     """
 
     def __init__(self, model, config: RunConfig, *, max_steps: int | None = None,
                  pool_dtype: str = "f16", device=None, group=None, fetch_ctas: int = 32,
                  fetch_threads: int = 32, fetch_priority: int = 0, hbm_layers: int = 0,
                  fetch_impl: str = "tma", fetch_rows: int = 16, dense: str = "tc",
-                 cuda_graph: bool = False, resident: bool = False):
+                 cuda_graph: bool = False, resident: bool = False, spec_stream: bool = True):
         config.validate()
         _lib.load()
         _enable_ieee_fp32()
@@ -230,6 +234,7 @@ class DecodeEngine:
             raise ValueError("resident needs the speculative scheme and hbm_layers=0")
         self.resident = bool(resident)
         self._res_valid = False
+        self.spec_stream_on = bool(spec_stream)
         self.scale = float(np.float32(1.0 / np.sqrt(d)))   # speculation.py:127
         self._load_weights(model)
         self._alloc()
@@ -326,6 +331,8 @@ class DecodeEngine:
         self.att_tickets = torch.zeros(tk.value, dtype=i32, device=dev)
         self.compute = torch.cuda.Stream(device=dev)
         self.fetch_stream = torch.cuda.Stream(device=dev, priority=self.fetch_priority)
+        self.spec_stream = torch.cuda.Stream(device=dev, priority=-1)
+        self.ev_q = [torch.cuda.Event() for _ in range(L)]
         self.ev_sel = [torch.cuda.Event() for _ in range(L)]
         self.ev_fetch = [torch.cuda.Event() for _ in range(L)]
         self.ev_att = [torch.cuda.Event() for _ in range(L)]
@@ -813,6 +820,10 @@ class DecodeEngine:
         sc = cfg.speculation
         C, Fs = self.compute, self.fetch_stream
         cs = C.cuda_stream
+        # speculation chain stream: its own (overlapping layer li's tail) unless traces
+        # read the scores per layer
+        SP = self.spec_stream if (self.spec_stream_on and not cfg.record_scores) else C
+        sps = SP.cuda_stream
         s = self.s_host
         graph = self._graph_mode
         recording = (cfg.record_selection or cfg.record_scores) and not graph
@@ -849,28 +860,35 @@ class DecodeEngine:
                 g1, b1, g2, b2 = self.ln[li]
                 _lib.call("ig_layernorm", x.data_ptr(), g1.data_ptr(), b1.data_ptr(),
                           float(spec.ln_eps), B, self.D, self.x_a.data_ptr(), cs)
+                if speculative and li >= 1 and SP is not C:
+                    # spec(li) done: qspec is free for the fused GEMM, idx/n/plan of li ready
+                    C.wait_event(self.ev_sel[li])
                 nxt = li + 1
                 if nxt < L:
                     if speculative:
                         # q/k/v of this layer + the speculation query of the next
                         self._gemm(self.x_a, self.wfused[li], self.qkvq, cs)
-                        self._mark("rehearse", nxt, C, True)
+                        if SP is not C:
+                            self.ev_q[li].record(C)
+                            SP.wait_event(self.ev_q[li])
+                        self._mark("rehearse", nxt, SP, True)
                         _lib.call("ig_rehearse_count", self.qspec.data_ptr(), self.qkvq.stride(0),
                                   self.cols[nxt].data_ptr(), self.pk[nxt - 1].data_ptr(),
                                   self.st.data_ptr(), B, Hg, d, self.kcols, self.S_max,
                                   self.scale, float(sc.alpha), self.scores.data_ptr(),
                                   self.maxkey.data_ptr(), self.rtickets.data_ptr(),
-                                  self.counts.data_ptr(), self.count_sum[nxt].data_ptr(), cs)
-                        self._mark("rehearse", nxt, C, False)
-                        self._mark("select", nxt, C, True)
+                                  self.counts.data_ptr(), self.count_sum[nxt].data_ptr(), sps)
+                        self._mark("rehearse", nxt, SP, False)
+                        self._mark("select", nxt, SP, True)
                         if self.world > 1:
-                            dist.all_reduce(self.count_sum[nxt], group=self.group)
+                            with torch.cuda.stream(SP):
+                                dist.all_reduce(self.count_sum[nxt], group=self.group)
                         _lib.call("ig_select", self.scores.data_ptr(),
                                   self.count_sum[nxt].data_ptr(), self.st.data_ptr(), B, Hg,
                                   self.H, self.S_max, self.cap, float(sc.cap_ratio),
                                   int(sc.min_select), self.idx[nxt].data_ptr(),
-                                  self.n[nxt].data_ptr(), self.err.data_ptr(), cs)
-                        self._mark("select", nxt, C, False)
+                                  self.n[nxt].data_ptr(), self.err.data_ptr(), sps)
+                        self._mark("select", nxt, SP, False)
                         if cfg.record_scores:
                             spec_scores[nxt] = self.scores[:, :, :s].cpu()
                         if resident:
@@ -881,8 +899,8 @@ class DecodeEngine:
                                       self.slot_used[nxt - 1].data_ptr(), B, Hg, self.cap,
                                       self.frow[par].data_ptr(), self.fslot[par].data_ptr(),
                                       self.fcount[par].data_ptr(),
-                                      self.moved_rows[nxt].data_ptr(), cs)
-                        self.ev_sel[nxt].record(C)
+                                      self.moved_rows[nxt].data_ptr(), sps)
+                        self.ev_sel[nxt].record(SP)
                         Fs.wait_event(self.ev_sel[nxt])
                         self._mark("fetch", nxt, Fs, True)
                         if resident:
