@@ -316,7 +316,7 @@ class DecodeEngine:
         if self.resident:
             self._alloc_resident()
         # skinny-GEMM workspace: the largest ceil(N/128) * ksplit * B * 128 over the projections
-        shapes = [(3 * Hg * d, D), (Hg * d, D), (D, Hg * d), (F, D), (D, F)]   # (N, K)
+        shapes = [(4 * Hg * d, D), (3 * Hg * d, D), (Hg * d, D), (D, Hg * d), (F, D), (D, F)]   # (N, K)
         ws = 0
         self.gemm_ksplit = {}
         for N_, K_ in shapes:

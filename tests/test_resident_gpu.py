@@ -264,3 +264,67 @@ def test_graph_replay_interleaved_with_eager_steps():
         finally:
             eng.close()
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+def test_set_resident_toggles_mid_run():
+    """bench.py's refetch variant switches a resident engine to refetch mode and
+    back mid-run: the decode must equal an engine that never switched."""
+    from paper_2406_19707_b200 import DecodeEngine
+    _, sk = models("m256")
+    ocfg = run_config("spec_counter", gen_len=10)
+    sessions = oracle_sessions(sk, ocfg)
+    outs = []
+    for toggle in (False, True):
+        eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg, record_selection=False),
+                                         copy.deepcopy(sessions), pool_dtype="f32", resident=True)
+        try:
+            o = []
+            for i in range(ocfg.gen_len):
+                if toggle and i in (3, 6):
+                    eng.set_resident(i == 6)
+                o.append(eng.decode_step().cpu().numpy())
+            outs.append(np.stack(o))
+        finally:
+            eng.close()
+    np.testing.assert_allclose(outs[0], outs[1], rtol=1e-5, atol=1e-5)
+
+
+def test_spec_stream_matches_single_stream():
+    """The speculation chain on its own stream gives the decode of the
+    single-stream schedule, bit for bit."""
+    from paper_2406_19707_b200 import DecodeEngine
+    _, sk = models("m256")
+    ocfg = run_config("spec_lru", gen_len=8)
+    sessions = oracle_sessions(sk, ocfg)
+    outs = []
+    for sp in (False, True):
+        eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg, record_selection=False),
+                                         copy.deepcopy(sessions), pool_dtype="f16", resident=True,
+                                         spec_stream=sp)
+        try:
+            outs.append(np.stack([eng.decode_step().cpu().numpy() for _ in range(ocfg.gen_len)]))
+        finally:
+            eng.close()
+    np.testing.assert_array_equal(outs[0], outs[1])
+
+
+def test_llama_like_ffn_narrower_than_fused_qkv():
+    """ffn_dim < 4 * model_dim (Llama-2 shape: 11008 vs 16384): the fused
+    [W_QKV | W_Q(next)] GEMM is the widest projection and sizes the split-K
+    workspace.  Selections identical to the oracle's, outputs within 1e-4."""
+    from paper_2406_19707_b200 import DecodeEngine
+    spec = O.ModelSpec(layers=3, model_dim=256, heads=2, ffn_dim=640, outlier_channels=8,
+                       outlier_scale=2.0, seed=5)
+    sk = O.skew_model(O.generate_synthetic(spec), calib_seed=0)
+    ocfg = O.RunConfig(scheme="speculative", prompt_len=40, gen_len=5, batch=2, record_selection=True)
+    sessions = oracle_sessions(sk, ocfg)
+    eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg), copy.deepcopy(sessions), pool_dtype="f32",
+                                     resident=True)
+    try:
+        ref_out, ref_recs = oracle_decode(sessions, ocfg.gen_len)
+        got = np.stack([eng.x.cpu().numpy()] + [eng.decode_step().cpu().numpy()
+                                                for _ in range(ocfg.gen_len)], axis=1)
+        assert _scaled_err(got, ref_out) < 1e-4
+        _cmp_records(eng.records, ref_recs, ocfg.batch, exact=True)
+    finally:
+        eng.close()
