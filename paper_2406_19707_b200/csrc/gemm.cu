@@ -397,6 +397,181 @@ sgemm_tc_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ 
   if (tid == 0 && ksplit > 1) tickets[tile] = 0;
 }
 
+// Swapped-operand variant: D^T = W^T . X^T, i.e. the weight tile is the MMA's
+// A operand (M = output columns) and x the B operand (N = 8 sequences per n
+// tile).  A warp owns 32 columns (two m16 tiles) and column m of m-tile mt
+// lives at physical column 4 (m % 8) + 2 mt + m / 8 of its 32, so one LDS.128
+// at (row k, column 4g) returns the A-fragment pair (g, g + 8) of both m-tiles
+// -- one shared load per four weights instead of four (the LDS / MIO queue
+// was a top stall of sgemm_tc_kernel).  Same pipeline, K split in two warp
+// groups (KIN = 2), split precision and merge as sgemm_tc_kernel.
+template <int NB, int STAGES>   // NB = 8-sequence n tiles (M <= 8 * NB)
+__global__ void __launch_bounds__(kGemmWarps * 32, (NB <= 2 ? 3 : 2))
+sgemm_tcw_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ W, int ldw,
+                 float* __restrict__ Y, int ldy, const float* __restrict__ R, int ldr, int M, int N,
+                 int K, int ksplit, int epilogue, float* __restrict__ ws,
+                 int32_t* __restrict__ tickets) {
+  extern __shared__ __align__(128) float smem[];
+  constexpr int MT = 8 * NB;
+  constexpr int kWs = kGemmKT * kTcWPitch, kXs = MT * kTcXPitch, kStage = kWs + kXs;
+  __shared__ int last;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int tile = blockIdx.x, ks = blockIdx.y;
+  const int ncol0 = tile * kGemmTileN;
+  const int chunks_all = (K + kGemmKT - 1) / kGemmKT;
+  const int cper = (chunks_all + ksplit - 1) / ksplit;
+  const int c0 = ks * cper, c1 = min(chunks_all, c0 + cper);
+  const int nch = max(0, c1 - c0);
+
+  StageLoader<MT> ld;
+  ld.init(W, ldw, X, ldx, M, N, K, c0, ncol0, kTcWPitch, kTcXPitch, kWs);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  auto load_stage = [&](int c, int st) { ld.load(c, sbase + st * kStage * 4, kTcWPitch); };
+
+  float big[2][NB][4], small[2][NB][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) big[mt][nb][i] = small[mt][nb][i] = 0.f;
+
+#pragma unroll
+  for (int i = 0; i < STAGES - 1; ++i) {
+    if (i < nch) load_stage(i, i);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  const int wc = (w & 3) * 32;                 // my 32 columns of the tile
+  const int k8lo = (w >> 2) * 16;              // my two k8 steps of each stage
+  for (int c = 0; c < nch; ++c) {
+    const int st = c % STAGES;
+    asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 2) : "memory");
+    __syncthreads();
+    const int nx = c + STAGES - 1;
+    if (nx < nch) load_stage(nx, nx % STAGES);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const float* ws_ = smem + st * kStage;
+    const float* xs_ = ws_ + kWs;
+#pragma unroll
+    for (int kq = 0; kq < kGemmKT / 2; kq += 8) {
+      const int k8 = k8lo + kq;
+      // A (weights): rows k8+t and k8+t+4, physical columns 4g .. 4g+3
+      const float4 wlo = *reinterpret_cast<const float4*>(ws_ + (k8 + t) * kTcWPitch + wc + 4 * g);
+      const float4 whi = *reinterpret_cast<const float4*>(ws_ + (k8 + t + 4) * kTcWPitch + wc + 4 * g);
+      uint32_t ah[2][4], al[2][4];
+      split_tf32(wlo.x, ah[0][0], al[0][0]);   // m-tile 0: (g, k t), (g+8, k t)
+      split_tf32(wlo.y, ah[0][1], al[0][1]);
+      split_tf32(wlo.z, ah[1][0], al[1][0]);   // m-tile 1
+      split_tf32(wlo.w, ah[1][1], al[1][1]);
+      split_tf32(whi.x, ah[0][2], al[0][2]);   // k t+4
+      split_tf32(whi.y, ah[0][3], al[0][3]);
+      split_tf32(whi.z, ah[1][2], al[1][2]);
+      split_tf32(whi.w, ah[1][3], al[1][3]);
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        const float* xr = xs_ + (nb * 8 + g) * kTcXPitch + k8 + t;
+        uint32_t bh0, bl0, bh1, bl1;
+        split_tf32(xr[0], bh0, bl0);
+        split_tf32(xr[4], bh1, bl1);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          mma_tf32(small[mt][nb], al[mt], bh0, bh1);
+          mma_tf32(small[mt][nb], ah[mt], bl0, bl1);
+          mma_tf32(big[mt][nb], ah[mt], bh0, bh1);
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) big[mt][nb][i] += small[mt][nb][i];
+  {                            // k-group 1 hands its sums to k-group 0 (fixed order)
+    __syncthreads();
+    float* red = smem;         // [4 warps][2][NB][4][32 lanes]
+    constexpr int per = 2 * NB * 4;
+    if (w >= 4) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            red[(((w - 4) * per) + (mt * NB + nb) * 4 + i) * 32 + lane] = big[mt][nb][i];
+    }
+    __syncthreads();
+    if (w < 4) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            big[mt][nb][i] += red[((w * per) + (mt * NB + nb) * 4 + i) * 32 + lane];
+    }
+  }
+  const size_t tile_elems = (size_t)M * kGemmTileN;
+  float* part = ws + ((size_t)tile * ksplit + ks) * tile_elems;
+  if (w < 4) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        // C: (m = g, seq 2t / 2t+1) and (m = g + 8, seq 2t / 2t+1)
+        const int col0 = wc + 4 * g + 2 * mt, col1 = col0 + 1;
+        const int s0 = nb * 8 + 2 * t, s1 = s0 + 1;
+        if (s0 < M) {
+          part[(size_t)s0 * kGemmTileN + col0] = big[mt][nb][0];
+          part[(size_t)s0 * kGemmTileN + col1] = big[mt][nb][2];
+        }
+        if (s1 < M) {
+          part[(size_t)s1 * kGemmTileN + col0] = big[mt][nb][1];
+          part[(size_t)s1 * kGemmTileN + col1] = big[mt][nb][3];
+        }
+      }
+  }
+  if (ksplit == 1) {
+    __syncthreads();
+  } else {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(tickets + tile, 1) == ksplit - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+  }
+  const float* tp = ws + (size_t)tile * ksplit * tile_elems;
+  for (int e = tid; e < M * kGemmTileN; e += blockDim.x) {
+    const int m = e / kGemmTileN, n = ncol0 + (e % kGemmTileN);
+    if (n >= N) continue;
+    float s = 0.f;
+    for (int i = 0; i < ksplit; ++i) s += __ldcg(tp + (size_t)i * tile_elems + e);
+    if (epilogue == 1) s = fmaxf(s, 0.f);
+    else if (epilogue == 2) s = __fadd_rn(R[(size_t)m * ldr + n], s);
+    Y[(size_t)m * ldy + n] = s;
+  }
+  if (tid == 0 && ksplit > 1) tickets[tile] = 0;
+}
+
+template <int NB, int STAGES>
+int launch_sgemm_tcw(const float* X, int ldx, const float* W, int ldw, float* Y, int ldy,
+                     const float* R, int ldr, int M, int N, int K, int ksplit, int epilogue,
+                     float* ws, int32_t* tickets, cudaStream_t s) {
+  const int tiles = (N + kGemmTileN - 1) / kGemmTileN;
+  const size_t smem =
+      (size_t)STAGES * (kGemmKT * kTcWPitch + 8 * NB * kTcXPitch) * sizeof(float);
+  IG_CUDA_STATUS(cudaFuncSetAttribute(sgemm_tcw_kernel<NB, STAGES>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  sgemm_tcw_kernel<NB, STAGES><<<dim3(tiles, ksplit), kGemmWarps * 32, smem, s>>>(
+      X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, ws, tickets);
+  IG_LAUNCH_STATUS();
+  return IG_OK;
+}
+
 template <int MTILES, int STAGES, int KIN>
 int launch_sgemm_tc(const float* X, int ldx, const float* W, int ldw, float* Y, int ldy,
                     const float* R, int ldr, int M, int N, int K, int ksplit, int epilogue,
@@ -487,11 +662,19 @@ extern "C" int ig_sgemm_tc(const float* X, int ldx, const float* W, int ldw, flo
   if ((size_t)tiles * ksplit * M * kGemmTileN > workspace_floats) return IG_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   static const int variant = [] {
-    // tuning sweeps only (profiles/r01e_gemm_variants.md): 1 = (3 stages, KIN 2, default),
-    // 0 = (3 stages, KIN 1), 2 = (4 stages, KIN 1)
+    // tuning sweeps only (profiles/r01e_gemm_variants.md): 4 = swapped operands
+    // (sgemm_tcw_kernel, default), 1 = (3 stages, KIN 2), 0 = (3 stages, KIN 1),
+    // 2 = (4 stages, KIN 1)
     const char* v = getenv("IG_TC_VARIANT");
-    return v ? atoi(v) : 1;
+    return v ? atoi(v) : 4;
   }();
+  if (variant == 4) {
+    if (M <= 8)
+      return launch_sgemm_tcw<1, 3>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
+    if (M <= 16)
+      return launch_sgemm_tcw<2, 3>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
+    return launch_sgemm_tcw<4, 3>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
+  }
   if (M <= 16) {
     if (variant == 0)
       return launch_sgemm_tc<1, 3, 1>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
