@@ -594,6 +594,7 @@ attend512_tma_kernel(const float* __restrict__ q, int ldq, const float* __restri
 constexpr int kMmaWarps = 4;
 constexpr int kMmaTPW = 8;                                  // tiles per warp (default)
 constexpr int kMmaTileBytes = 16 * 512;
+constexpr int kMmaSlotBytes = kMmaTileBytes + 64;            // + the tile's 16 row ids
 
 template <typename T> struct MmaT;
 template <> struct MmaT<__half> {
@@ -674,7 +675,9 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
   const int crows = (((rows + nchunks - 1) / nchunks) + 63) & ~63;
   const int r0 = c * crows, r1 = min(rows, r0 + crows);
   const uint8_t* src = reinterpret_cast<const uint8_t*>(stage + bh * (size_t)cap * 2 * d);
-  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(att_ring) + w * RING * kMmaTileBytes;
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(att_ring) + w * RING * kMmaSlotBytes;
+  const int* ring_ids = reinterpret_cast<const int*>(att_ring + (size_t)w * RING * kMmaSlotBytes +
+                                                     kMmaTileBytes);
 
   // query split into NS parts: B fragments of the 8 k16-steps (column g < NS)
   uint32_t bq[8][2];
@@ -693,11 +696,12 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
 
-  // tile j of this warp: rows [tb, tb + 16), tb = r0 + (j * warps + w) * 16
-  int ids[TPW][2];
+  // tile j of this warp: rows [tb, tb + 16), tb = r0 + (j * warps + w) * 16; the
+  // tile's row ids ride in the same cp.async group (a separate global load of
+  // them was the kernel's top stall)
   auto issue = [&](int j) {
     const int tb = r0 + (j * kMmaWarps + w) * 16;
-    const uint32_t slot = ring + (j % RING) * kMmaTileBytes;
+    const uint32_t slot = ring + (j % RING) * kMmaSlotBytes;
 #pragma unroll
     for (int rr = 0; rr < 16; ++rr) {
       const int r = tb + rr;
@@ -707,12 +711,14 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
                    "l"(src + (size_t)(ok ? r : r0) * 512 + lane * 16), "r"(ok ? 16 : 0)
                    : "memory");
     }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int r = tb + g + 8 * u;
-      ids[j][u] = r < r1 ? (idx ? idx[bh * cap + r] : r) : -1;
+    if (idx != nullptr && lane < 16) {
+      const int r = tb + lane;
+      const bool ok = r < r1;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
+                   ::"r"(slot + kMmaTileBytes + lane * 4), "l"(idx + bh * cap + (ok ? r : r0)),
+                   "r"(ok ? 4 : 0) : "memory");
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
   };
   int ntiles = 0;
 #pragma unroll
@@ -731,7 +737,9 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncwarp();
-    const uint32_t slot = ring + (j % RING) * kMmaTileBytes;
+    const uint32_t slot = ring + (j % RING) * kMmaSlotBytes;
+    const int tb = r0 + (j * kMmaWarps + w) * 16;
+    const int* sid = ring_ids + (j % RING) * (kMmaSlotBytes / 4);
     // S = K . Qm (two accumulators: half-length dependency chains)
     float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
     const int lr = lane & 15, lh = lane >> 4;
@@ -748,8 +756,10 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
     s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
     s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
     s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
-    const bool ok0 = ids[j][0] >= 0 && ids[j][0] != pos;
-    const bool ok1 = ids[j][1] >= 0 && ids[j][1] != pos;
+    const int id0 = tb + g < r1 ? (idx ? sid[g] : tb + g) : -1;
+    const int id1 = tb + g + 8 < r1 ? (idx ? sid[g + 8] : tb + g + 8) : -1;
+    const bool ok0 = id0 >= 0 && id0 != pos;
+    const bool ok1 = id1 >= 0 && id1 != pos;
     s0 = ok0 ? s0 / sqrt_d : -INFINITY;                      // row g
     s1 = ok1 ? s1 / sqrt_d : -INFINITY;                      // row g + 8
     float tm = fmaxf(s0, s1);
@@ -918,7 +928,7 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
   do {                                                                                         \
     const int chunk = kMmaWarps * (TPW) * 16;                                                  \
     const dim3 g3((cap + chunk - 1) / chunk, grid.y, grid.z);                                  \
-    const size_t smem = (size_t)kMmaWarps * (RING) * kMmaTileBytes;                            \
+    const size_t smem = (size_t)kMmaWarps * (RING) * kMmaSlotBytes;                            \
     IG_CUDA_STATUS(cudaFuncSetAttribute(attend512_mma_kernel<T, RING, TPW>,                    \
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     attend512_mma_kernel<T, RING, TPW><<<g3, kMmaWarps * 32, smem, s>>>(                       \
