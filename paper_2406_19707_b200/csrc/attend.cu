@@ -886,6 +886,284 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
   if (threadIdx.x == 0) tickets[bh] = 0;
 }
 
+// ---------------------------------------------------------------------------
+// Warp-persistent variant of the tensor-core path (default).  Work items are
+// 128-row segments of a (b, h) row set; every warp owns a contiguous range of
+// items and streams their 16-row tiles through its own cp.async ring, issuing
+// the next item's first tile (with the item's query row) before it closes the
+// current item -- so the pipeline never drains between items and no CTA-wide
+// barrier exists.  A warp closes an item by writing its (m, l, acc) partial
+// and taking a per-(b, h) ticket; the last segment to finish merges all
+// segments in fixed order (deterministic).  At 819-row selections the
+// CTA-per-chunk kernel spent most of its time filling and draining its
+// pipeline once per 400-row chunk.
+// ---------------------------------------------------------------------------
+constexpr int kWpSeg = 128;                                  // rows per work item
+constexpr int kWpWarps = 4;
+constexpr int kWpSlotBytes = kMmaTileBytes + 64 + 512;       // rows + ids + query row
+
+template <typename T, int RING>
+__global__ void __launch_bounds__(kWpWarps * 32, 3)
+attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_cur,
+                    const float* __restrict__ v_cur, int ldkv, const T* __restrict__ stage,
+                    const int32_t* __restrict__ idx, const int32_t* __restrict__ n_in,
+                    const int32_t* __restrict__ rows_bh, const int32_t* __restrict__ pos_in,
+                    const ig_step_state* __restrict__ st, int B, int Hg, int cap, float sqrt_d,
+                    int max_chunks, float* __restrict__ partial, int32_t* __restrict__ tickets,
+                    float* __restrict__ out, int ldo) {
+  constexpr int d = 128, NS = MmaT<T>::NS;
+  extern __shared__ __align__(128) uint8_t wp_ring[];        // [warps][RING][slot]
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int maxseg = (cap + kWpSeg - 1) / kWpSeg;            // == max_chunks (scratch layout)
+  const long long items = (long long)B * Hg * maxseg;
+  const long long tw = (long long)gridDim.x * kWpWarps, gw = (long long)blockIdx.x * kWpWarps + w;
+  const long long per = (items + tw - 1) / tw;
+  const long long it_lo = gw * per, it_hi = min(items, it_lo + per);
+  uint8_t* wbase = wp_ring + (size_t)w * RING * kWpSlotBytes;
+  const uint32_t sring = (uint32_t)__cvta_generic_to_shared(wbase);
+
+  // item geometry; an item exists if seg < nseg(bh) (segment 0 always: the current row)
+  auto geom = [&](long long it, int& bh, int& seg, int& r0, int& r1, int& ntl) -> bool {
+    bh = (int)(it / maxseg);
+    seg = (int)(it - (long long)bh * maxseg);
+    const int b = bh / Hg;
+    const int rows = att_rows(rows_bh, n_in, st, b, (size_t)bh);
+    const int nseg = max(1, (rows + kWpSeg - 1) / kWpSeg);
+    if (seg >= nseg) return false;
+    r0 = seg * kWpSeg;
+    r1 = min(rows, r0 + kWpSeg);
+    ntl = max(0, (r1 - r0 + 15) / 16);
+    return true;
+  };
+  auto next_item = [&](long long it) -> long long {        // first existing item > it
+    for (long long j = it + 1; j < it_hi; ++j) {
+      int bh, seg, r0, r1, ntl;
+      if (geom(j, bh, seg, r0, r1, ntl)) return j;
+    }
+    return -1;
+  };
+  // issue tile `tl` of item (bh, r0, r1) into ring slot `slot_i`; tile 0 also
+  // brings the item's query row
+  auto issue = [&](int bh, int r0, int r1, int tl, int slot_i) {
+    const uint32_t slot = sring + slot_i * kWpSlotBytes;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(stage + (size_t)bh * cap * 2 * d);
+    const int tb = r0 + tl * 16;
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr) {
+      const int r = tb + rr;
+      const bool ok = r < r1;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;"
+                   ::"r"(slot + rr * 512 + ((lane ^ (rr & 7)) << 4)),
+                   "l"(src + (size_t)(ok ? r : 0) * 512 + lane * 16), "r"(ok ? 16 : 0)
+                   : "memory");
+    }
+    if (idx != nullptr && lane < 16) {
+      const int r = tb + lane;
+      const bool ok = r < r1;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;"
+                   ::"r"(slot + kMmaTileBytes + lane * 4),
+                   "l"(idx + (size_t)bh * cap + (ok ? r : 0)), "r"(ok ? 4 : 0) : "memory");
+    }
+    if (tl == 0) {
+      const int b = bh / Hg, h = bh - b * Hg;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                   ::"r"(slot + kMmaTileBytes + 64 + lane * 16),
+                   "l"(q + (size_t)b * ldq + (size_t)h * d + lane * 4) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  long long cur = -1;
+  {
+    int bh, seg, r0, r1, ntl;
+    if (it_lo < it_hi && geom(it_lo, bh, seg, r0, r1, ntl)) cur = it_lo;
+    else if (it_lo < it_hi) cur = next_item(it_lo);
+  }
+  int slot_ctr = 0;                     // ring slot of the next tile to issue
+  if (cur >= 0) {
+    int bh, seg, r0, r1, ntl;
+    geom(cur, bh, seg, r0, r1, ntl);
+    issue(bh, r0, r1, 0, 0);            // tile 0 (maybe empty: still carries q)
+    slot_ctr = 1;
+  }
+  int cslot = 0;                        // ring slot of the tile being computed
+  while (cur >= 0) {
+    int bh, seg, r0, r1, ntl;
+    geom(cur, bh, seg, r0, r1, ntl);
+    const int b = bh / Hg, h = bh - b * Hg;
+    const int pos = pos_in[bh];
+    const long long nxt = next_item(cur);
+    float m = -INFINITY, l = 0.f;
+    float acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    uint32_t bq[8][2];
+    const int ntiles = max(1, ntl);     // an empty item still consumes its q-carrying slot
+    for (int tl = 0; tl < ntiles; ++tl) {
+      // look ahead one tile: this item's next tile or the next item's first
+      bool issued = false;
+      if (tl + 1 < ntl) {
+        issue(bh, r0, r1, tl + 1, slot_ctr % RING);
+        issued = true;
+      } else if (nxt >= 0) {
+        int nbh, nseg, nr0, nr1, nntl;
+        geom(nxt, nbh, nseg, nr0, nr1, nntl);
+        issue(nbh, nr0, nr1, 0, slot_ctr % RING);
+        issued = true;
+      }
+      if (issued) {
+        ++slot_ctr;
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncwarp();
+      const uint32_t slot = sring + cslot * kWpSlotBytes;
+      const uint8_t* gslot = wbase + (size_t)cslot * kWpSlotBytes;
+      if (tl == 0) {                    // the item's query row -> split B fragments
+        const float* qs = reinterpret_cast<const float*>(gslot + kMmaTileBytes + 64);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const int k0 = kk * 16 + 2 * t;
+          bq[kk][0] = MmaT<T>::pack(split_part<T>(qs[k0], g), split_part<T>(qs[k0 + 1], g));
+          bq[kk][1] = MmaT<T>::pack(split_part<T>(qs[k0 + 8], g), split_part<T>(qs[k0 + 9], g));
+          if (g >= NS) bq[kk][0] = bq[kk][1] = 0u;
+        }
+      }
+      if (tl < ntl) {
+        const int tb = r0 + tl * 16;
+        const int* sid = reinterpret_cast<const int*>(gslot + kMmaTileBytes);
+        float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        const int lr = lane & 15, lh = lane >> 4;
+        const uint32_t rowaddr = slot + lr * 512;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          uint32_t a[4];
+          ldsm_x4(rowaddr + (((2 * kk + lh) ^ (lr & 7)) << 4), a);
+          MmaT<T>::mma(sc[kk & 1], a, bq[kk][0], bq[kk][1]);
+        }
+        float s0 = (sc[0][0] + sc[1][0]) + (sc[0][1] + sc[1][1]);
+        float s1 = (sc[0][2] + sc[1][2]) + (sc[0][3] + sc[1][3]);
+        s0 += __shfl_xor_sync(0xffffffffu, s0, 1);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+        s0 += __shfl_xor_sync(0xffffffffu, s0, 2);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, 2);
+        const int id0 = tb + g < r1 ? (idx ? sid[g] : tb + g) : -1;
+        const int id1 = tb + g + 8 < r1 ? (idx ? sid[g + 8] : tb + g + 8) : -1;
+        s0 = (id0 >= 0 && id0 != pos) ? s0 / sqrt_d : -INFINITY;
+        s1 = (id1 >= 0 && id1 != pos) ? s1 / sqrt_d : -INFINITY;
+        float tm = fmaxf(s0, s1);
+        tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 4));
+        tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 8));
+        tm = fmaxf(tm, __shfl_xor_sync(0xffffffffu, tm, 16));
+        if (tm != -INFINITY) {
+          if (tm > m) {
+            const float corr = expf(m - tm);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              acc[i][0] *= corr; acc[i][1] *= corr; acc[i][2] *= corr; acc[i][3] *= corr;
+            }
+            l *= corr;
+            m = tm;
+          }
+          const float p0 = expf(s0 - m), p1 = expf(s1 - m);
+          l += p0 + p1;
+          const float pa = __shfl_sync(0xffffffffu, p0, 8 * t);
+          const float pb = __shfl_sync(0xffffffffu, p0, 8 * t + 4);
+          const float pc = __shfl_sync(0xffffffffu, p1, 8 * t);
+          const float pd = __shfl_sync(0xffffffffu, p1, 8 * t + 4);
+          uint32_t pb0 = MmaT<T>::pack(split_part<T>(pa, g), split_part<T>(pb, g));
+          uint32_t pb1 = MmaT<T>::pack(split_part<T>(pc, g), split_part<T>(pd, g));
+          if (g >= NS) pb0 = pb1 = 0u;
+          const int vr = (lane & 7) + ((lane >> 4) << 3), vc = (lane >> 3) & 1;
+          const uint32_t vaddr = slot + vr * 512;
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt) {
+            uint32_t a[4];
+            ldsm_x4_t(vaddr + (((16 + 2 * mt + vc) ^ (vr & 7)) << 4), a);
+            MmaT<T>::mma(acc[mt], a, pb0, pb1);
+          }
+        }
+      }
+      __syncwarp();
+      cslot = (cslot + 1) % RING;
+    }
+    if (seg == 0) {                     // the current token: GPU-resident f32 row, f32 dot
+      const float* qr = q + (size_t)b * ldq + (size_t)h * d;
+      const float* kr = k_cur + (size_t)b * ldkv + (size_t)h * d;
+      float dot = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dot = fmaf(qr[lane * 4 + i], kr[lane * 4 + i], dot);
+      dot = warp_sum(dot);
+      const float scur = dot / sqrt_d;
+      if (scur > m) {
+        const float corr = expf(m - scur);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          acc[i][0] *= corr; acc[i][1] *= corr; acc[i][2] *= corr; acc[i][3] *= corr;
+        }
+        l *= corr;
+        m = scur;
+      }
+      const float p = expf(scur - m);
+      if (g == 0) l += p;
+      if (t == 0) {
+        const float* vrow = v_cur + (size_t)b * ldkv + (size_t)h * d;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+          acc[mt][0] = fmaf(p, vrow[mt * 16 + g], acc[mt][0]);
+          acc[mt][2] = fmaf(p, vrow[mt * 16 + g + 8], acc[mt][2]);
+        }
+      }
+    }
+    // close the item: partial (m, l, acc) of segment seg
+    l += __shfl_xor_sync(0xffffffffu, l, 4);
+    l += __shfl_xor_sync(0xffffffffu, l, 8);
+    l += __shfl_xor_sync(0xffffffffu, l, 16);
+    float* part = partial + ((size_t)bh * max_chunks + seg) * (size_t)(d + 2);
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      float y0 = acc[mt][0] + acc[mt][1], y1 = acc[mt][2] + acc[mt][3];
+      y0 += __shfl_xor_sync(0xffffffffu, y0, 1);
+      y1 += __shfl_xor_sync(0xffffffffu, y1, 1);
+      y0 += __shfl_xor_sync(0xffffffffu, y0, 2);
+      y1 += __shfl_xor_sync(0xffffffffu, y1, 2);
+      if (t == 0) {
+        part[2 + mt * 16 + g] = y0;
+        part[2 + mt * 16 + g + 8] = y1;
+      }
+    }
+    if (lane == 0) { part[0] = m; part[1] = l; }
+    __threadfence();
+    __syncwarp();
+    const int rows = att_rows(rows_bh, n_in, st, b, (size_t)bh);
+    const int nseg = max(1, (rows + kWpSeg - 1) / kWpSeg);
+    int lastw = 0;
+    if (lane == 0) lastw = atomicAdd(tickets + bh, 1) == nseg - 1;
+    lastw = __shfl_sync(0xffffffffu, lastw, 0);
+    if (lastw) {                        // merge every segment of (b, h) in order
+      __threadfence();
+      const float* pb = partial + (size_t)bh * max_chunks * (d + 2);
+      float MM = -INFINITY;
+      for (int i = 0; i < nseg; ++i) MM = fmaxf(MM, __ldcg(pb + (size_t)i * (d + 2)));
+      float LL = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int i = 0; i < nseg; ++i) {
+        const float mi = __ldcg(pb + (size_t)i * (d + 2));
+        const float sc = mi == -INFINITY ? 0.f : expf(mi - MM);
+        LL += __ldcg(pb + (size_t)i * (d + 2) + 1) * sc;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) o[e] += __ldcg(pb + (size_t)i * (d + 2) + 2 + lane * 4 + e) * sc;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) out[(size_t)b * ldo + (size_t)h * d + lane * 4 + e] = o[e] / LL;
+      if (lane == 0) tickets[bh] = 0;
+    }
+    cur = nxt;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // IG_ATTEND_IMPL=tma selects the TMA-fed 512-B path.  Measured alone at C3
 // (round 1): register-fed 2.84 TB/s vs TMA-fed 2.39 TB/s -- the per-row math
 // (f16 unpack + shuffle reductions), not the feed, bounds this kernel, so
@@ -918,12 +1196,17 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
       return IG_OK;
     }
     if (d == 128 && attend_impl() == 'm') {  // 512-B rows on the tensor cores (default)
-      // tuning sweeps only (IG_ATT_VARIANT): 0 = ring 2 x 8 tiles/warp (3 CTAs/SM, default),
-      // 1 = ring 2 x 4 tiles, 2 = ring 3 x 8 tiles (2 CTAs/SM), 3 = ring 2 x 16 tiles
-      static const int variant = [] {
+      // IG_ATT_VARIANT (tuning sweeps): 0 = CTA per chunk, ring 2 x 8 tiles/warp (3 CTAs/SM),
+      // 1 = ring 2 x 4 tiles, 2 = ring 3 x 8 tiles (2 CTAs/SM), 3 = ring 2 x 16 tiles,
+      // 4 = warp-persistent (attend512_wp_kernel)
+      static const int forced = [] {
         const char* v = getenv("IG_ATT_VARIANT");
-        return v ? atoi(v) : 0;
+        return v ? atoi(v) : -1;
       }();
+      // default: warp-persistent for short row sets (selections of <= 2K rows, where
+      // the CTA kernel's per-chunk pipeline fill dominates), CTA-per-chunk otherwise
+      // (tools/attend_probe.py: 819 rows 4.07 vs 3.75 TB/s; 4K-32K rows 5.8-6.0 vs 5.2-5.5)
+      const int variant = forced >= 0 ? forced : (cap <= 2048 ? 4 : 0);
 #define IG_ATT_MMA(RING, TPW)                                                                  \
   do {                                                                                         \
     const int chunk = kMmaWarps * (TPW) * 16;                                                  \
@@ -935,6 +1218,26 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
         q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, Hg, cap, sqrt_d, \
         max_chunks, partial, tickets, out, ldo);                                               \
   } while (0)
+      if (variant == 4) {   // warp-persistent
+        static int sms = 0;
+        if (sms == 0) {
+          int dev = 0;
+          if (cudaGetDevice(&dev) != cudaSuccess ||
+              cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            sms = 148;
+        }
+        const int maxseg = (cap + kWpSeg - 1) / kWpSeg;
+        const long long items = (long long)grid.z * grid.y * maxseg;
+        const int ctas = (int)min((long long)sms * 3, (items + kWpWarps - 1) / kWpWarps);
+        const size_t smem = (size_t)kWpWarps * 2 * kWpSlotBytes;
+        IG_CUDA_STATUS(cudaFuncSetAttribute(attend512_wp_kernel<T, 2>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attend512_wp_kernel<T, 2><<<ctas, kWpWarps * 32, smem, s>>>(
+            q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, (int)grid.z,
+            (int)grid.y, cap, sqrt_d, max_chunks, partial, tickets, out, ldo);
+        IG_LAUNCH_STATUS();
+        return IG_OK;
+      }
       switch (variant) {
         case 1: IG_ATT_MMA(2, 4); break;
         case 2: IG_ATT_MMA(3, 8); break;
