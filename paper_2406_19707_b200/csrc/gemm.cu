@@ -424,7 +424,7 @@ sgemm_tc_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ 
 // was a top stall of sgemm_tc_kernel).  Same pipeline, K split in two warp
 // groups (KIN = 2), split precision and merge as sgemm_tc_kernel.
 template <int NB, int STAGES>   // NB = 8-sequence n tiles (M <= 8 * NB)
-__global__ void __launch_bounds__(kGemmWarps * 32, (NB <= 2 ? 3 : 2))
+__global__ void __launch_bounds__(kGemmWarps * 32, (NB <= 2 && STAGES <= 3 ? 3 : 2))
 sgemm_tcw_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ W, int ldw,
                  float* __restrict__ Y, int ldy, const float* __restrict__ R, int ldr, int M, int N,
                  int K, int ksplit, int epilogue, float* __restrict__ ws,
@@ -653,15 +653,14 @@ extern "C" int ig_sgemm_rows(const float* X, int ldx, const float* W, int ldw, f
 }
 
 extern "C" int ig_sgemm_tc_ksplit(int M, int N, int K) {
-  // Measured (tools/gemm_probe.py --ksplit all, C3 shapes, profiles/r01b_gemm_probe.jsonl):
-  // ~1900 CTAs (>= 4 waves of 3 CTAs/SM) beat the wave-filling rule of
-  // ig_sgemm_rows_ksplit by 5-15%, as long as each CTA keeps >= 10 chunks
-  // (profiles/r01e_gemm_variants.md).
+  // Measured for sgemm_tcw_kernel (tools/gemm_probe.py --ksplit all, C3 shapes,
+  // profiles/r01g_gemm_ksplit_tcw.jsonl): ~1200 CTAs, at most 16 splits and >= 10
+  // pipeline chunks per CTA come within noise of the best split of every shape.
   (void)M;
   const int tiles = (N + ig::kGemmTileN - 1) / ig::kGemmTileN;
   const int chunks = (K + ig::kGemmKT - 1) / ig::kGemmKT;
-  int ks = (1920 + tiles - 1) / tiles;
-  if (ks > 32) ks = 32;
+  int ks = (1200 + tiles - 1) / tiles;        // ~1200 CTAs: ~3 waves of 3 CTAs/SM
+  if (ks > 16) ks = 16;
   if (ks > chunks / 10) ks = chunks / 10;     // >= 10 pipeline chunks per CTA
   return ks < 1 ? 1 : ks;
 }
@@ -686,7 +685,11 @@ extern "C" int ig_sgemm_tc(const float* X, int ldx, const float* W, int ldw, flo
     const char* v = getenv("IG_TC_VARIANT");
     return v ? atoi(v) : 4;
   }();
-  if (variant == 4) {
+  if (variant == 5 && M > 8 && M <= 16)     // sweep: 4 stages, 2 CTAs/SM
+    return launch_sgemm_tcw<2, 4>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
+  if (variant == 6 && M > 8 && M <= 16)     // sweep: 5 stages, 2 CTAs/SM
+    return launch_sgemm_tcw<2, 5>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
+  if (variant == 4 || variant >= 5) {
     if (M <= 8)
       return launch_sgemm_tcw<1, 3>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
     if (M <= 16)

@@ -26,7 +26,8 @@ def main():
     lib = _lib.load()
     sh = SHAPES[a.shape]
     D, F, M = sh["model_dim"], sh["ffn_dim"], a.batch
-    shapes = {"qkv": (3 * D, D), "wo": (D, D), "ffn_in": (F, D), "ffn_out": (D, F)}
+    shapes = {"fused_qkv_qspec": (4 * D, D), "qkv": (3 * D, D), "wo": (D, D), "ffn_in": (F, D),
+              "ffn_out": (D, F)}
     if a.only:
         n_, k_ = (int(v) for v in a.only.split(","))
         shapes = {"only": (n_, k_)}
