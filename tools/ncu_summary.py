@@ -56,9 +56,14 @@ def launches(path, steps):
         per[k][1] += ms
         by_stream[r[si]] += ms
         total += ms
+    big = {s: ms for s, ms in by_stream.items() if ms >= 0.05 * total}
+    rest = total - sum(big.values())
+    streams = ", ".join(f"stream {s}: {ms / steps:.1f} ms/step" for s, ms in sorted(big.items()))
+    if rest > 0:
+        streams += (f", {len(by_stream) - len(big)} more streams (graph-replay side "
+                    f"streams): {rest / steps:.1f} ms/step")
     out = [f"{sum(c for c, _ in per.values())} launches, {total:.1f} ms of serialised device time "
-           f"for {steps} steps; by stream: " + ", ".join(f"stream {s}: {ms / steps:.1f} ms/step"
-                                                         for s, ms in sorted(by_stream.items())), "",
+           f"for {steps} steps; by stream: " + streams, "",
            "| share | ms / step | launches / step | kernel |", "|---:|---:|---:|---|"]
     for k, (c, ms) in sorted(per.items(), key=lambda x: -x[1][1]):
         out.append(f"| {100 * ms / total:.1f}% | {ms / steps:.2f} | {c // steps} | `{k}` |")

@@ -3,7 +3,7 @@
 # OPT-13B shape: identical launches, short setup).  Usage: tools/profile_kernels.sh r01c [kernels...]
 R=${1:-r01c}
 shift
-KS=${@:-"fetch_slots_kernel rehearse_count_kernel attend512_mma_kernel select_kernel append_kernel sgemm_tc_kernel resident_plan_kernel"}
+KS=${@:-"fetch_slots_kernel rehearse_count_kernel attend512_wp_kernel attend512_mma_kernel select_kernel append_kernel sgemm_tcw_kernel resident_plan_kernel layernorm_kernel"}
 export IG_PROFILE_WINDOW=1
 for K in $KS; do
   ncu --profile-from-start off --set full --clock-control none --import-source on \
