@@ -46,7 +46,7 @@ UNIT = "tok/s"
 def _args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--batch", type=int, default=WORKLOAD["batch"])
@@ -64,6 +64,8 @@ def _args():
     ap.add_argument("--no-resident", dest="resident", action="store_false",
                     help="refetch every selected row each step (the reference's data movement) "
                          "instead of keeping each layer's fetched set resident in HBM")
+    ap.add_argument("--append-stream", action="store_true",
+                    help="run ig_append beside the attention on its own stream (measured neutral)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo lets N ranks share one GPU (tests of the N > 1 path)")
     ap.add_argument("--no-variant", "--no-hbm-variant", dest="no_variant", action="store_true",
@@ -254,7 +256,7 @@ def run_b200(a) -> None:
     eng = DecodeEngine(model, cfg, pool_dtype="f16", device=dev, group=group, fetch_ctas=a.fetch_ctas,
                        fetch_threads=a.fetch_threads, fetch_priority=a.fetch_priority,
                        fetch_impl=a.fetch_impl, fetch_rows=a.fetch_rows, dense=a.dense,
-                       cuda_graph=a.cuda_graph, resident=a.resident)
+                       cuda_graph=a.cuda_graph, resident=a.resident, append_stream=a.append_stream)
     # engine holds its own (sharded) copies: drop the full model
     del model
     torch.cuda.empty_cache()

@@ -169,8 +169,10 @@ int ig_touch(const int32_t* idx, const int32_t* n, int cap, const ig_step_state*
 /* ---- K4 attend: replaces attention_head on the fetched set (model.py:156-180,
  * engine.py:352-358).  Per (b, h): softmax((q . K^T) / float32(sqrt(d))) . V
  * over stage rows r < n (n == NULL -> s rows, idx == NULL -> row r) whose row
- * index != pos, plus the GPU-resident current row (k_cur, v_cur).  Split
- * over row chunks; partial/ticket are scratch sized by ig_attend_scratch.   */
+ * index != pos, plus the GPU-resident current row (k_cur, v_cur).  pos ==
+ * NULL means pos = st->s_len for every (b, h) (the append position when no
+ * pool limit applies).  Split over row chunks; partial/ticket are scratch
+ * sized by ig_attend_scratch.                                              */
 int ig_attend_scratch(int B, int Hg, int d, int cap, size_t* partial_floats,
                       size_t* tickets);
 int ig_attend(const float* q, int ldq, const float* k_cur, const float* v_cur, int ldkv,

@@ -19,6 +19,14 @@ constexpr int kAttChunk = 128;     // staged rows per CTA
 constexpr int kAttMaxPer = 8;      // head_dim <= 256
 constexpr int kAttRowsInFlight = 4;
 
+// The current token's pool row: pos_in[b, h] (what ig_append chose), or, with
+// pos_in == NULL, the append position below the pool limit (st->s_len) --
+// which lets the append run concurrently with the attention when no pool
+// limit can make it evict.
+__device__ __forceinline__ int att_pos(const int32_t* pos_in, const ig_step_state* st, size_t bh) {
+  return pos_in ? pos_in[bh] : st->s_len;
+}
+
 // Rows of one (b, h): a per-head count (resident slot tables), the step's
 // shared n (selection), or every pool row (identity, layer 0).
 __device__ __forceinline__ int att_rows(const int32_t* rows_bh, const int32_t* n_in,
@@ -58,7 +66,7 @@ attend_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_
   const int nchunks = max(1, (rows + kAttChunk - 1) / kAttChunk);
   if (c >= nchunks) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int pos = pos_in[bh];
+  const int pos = att_pos(pos_in, st, bh);
 
   float qv[P];
   {
@@ -213,7 +221,7 @@ attend512_kernel(const float* __restrict__ q, int ldq, const float* __restrict__
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool klane = lane < 16;
   const int e0 = (lane & 15) * 8;       // first of my 8 elements (K or V)
-  const int pos = pos_in[bh];
+  const int pos = att_pos(pos_in, st, bh);
 
   float qv[8];
   {
@@ -419,7 +427,7 @@ attend512_tma_kernel(const float* __restrict__ q, int ldq, const float* __restri
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const bool klane = lane < 16;
   const int e0 = (lane & 15) * 8;
-  const int pos = pos_in[bh];
+  const int pos = att_pos(pos_in, st, bh);
   const int r0 = c * kTmaChunk, r1 = min(rows, r0 + kTmaChunk);
   const int nst = (r1 - r0 + kTmaRows - 1) / kTmaRows;   // stages of this chunk (may be 0)
   const uint8_t* src = reinterpret_cast<const uint8_t*>(stage + bh * (size_t)cap * 2 * d);
@@ -670,7 +678,7 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
   if (c >= nchunks) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int pos = pos_in[bh];
+  const int pos = att_pos(pos_in, st, bh);
   // balanced chunks: nchunks of at most warps*TPW*16 rows, sizes within one 64-row tile group
   const int crows = (((rows + nchunks - 1) / nchunks) + 63) & ~63;
   const int r0 = c * crows, r1 = min(rows, r0 + crows);
@@ -992,7 +1000,7 @@ attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restric
     int bh, seg, r0, r1, ntl;
     geom(cur, bh, seg, r0, r1, ntl);
     const int b = bh / Hg, h = bh - b * Hg;
-    const int pos = pos_in[bh];
+    const int pos = att_pos(pos_in, st, bh);
     const long long nxt = next_item(cur);
     float m = -INFINITY, l = 0.f;
     float acc[8][4];
@@ -1291,7 +1299,7 @@ static int attend_dispatch(const float* q, int ldq, const float* k_cur, const fl
                            const int32_t* n, const int32_t* rows_bh, const int32_t* pos,
                            const ig_step_state* st, int B, int Hg, int d, int cap, float* partial,
                            int32_t* tickets, float* out, int ldo, void* stream) {
-  if (!q || !k_cur || !v_cur || !stage || !pos || !st || !partial || !tickets || !out || B < 1 ||
+  if (!q || !k_cur || !v_cur || !stage || !st || !partial || !tickets || !out || B < 1 ||
       Hg < 1 || d < 1 || d > 32 * kAttMaxPer || cap < 1 || ldq < Hg * d || ldkv < Hg * d ||
       ldo < Hg * d)
     return IG_EINVAL;

@@ -423,8 +423,8 @@ sgemm_tc_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ 
 // -- one shared load per four weights instead of four (the LDS / MIO queue
 // was a top stall of sgemm_tc_kernel).  Same pipeline, K split in two warp
 // groups (KIN = 2), split precision and merge as sgemm_tc_kernel.
-template <int NB, int STAGES>   // NB = 8-sequence n tiles (M <= 8 * NB)
-__global__ void __launch_bounds__(kGemmWarps * 32, (NB <= 2 && STAGES <= 3 ? 3 : 2))
+template <int NB, int STAGES, int KG>   // NB = 8-sequence n tiles (M <= 8 * NB); KG k-groups
+__global__ void __launch_bounds__(kGemmWarps * 32, (NB <= 2 && STAGES <= 3 && KG <= 2 ? 3 : 2))
 sgemm_tcw_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ W, int ldw,
                  float* __restrict__ Y, int ldy, const float* __restrict__ R, int ldr, int M, int N,
                  int K, int ksplit, int epilogue, float* __restrict__ ws,
@@ -432,6 +432,9 @@ sgemm_tcw_kernel(const float* __restrict__ X, int ldx, const float* __restrict__
   extern __shared__ __align__(128) float smem[];
   constexpr int MT = 8 * NB;
   constexpr int kWs = kGemmKT * kTcWPitch, kXs = MT * kTcXPitch, kStage = kWs + kXs;
+  constexpr int WPG = kGemmWarps / KG;         // warps per k-group
+  constexpr int HV = 4 / WPG;                  // 32-column halves per warp (1 or 2)
+  constexpr int MTW = 2 * HV;                  // m16 tiles per warp
   __shared__ int last;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -447,9 +450,9 @@ sgemm_tcw_kernel(const float* __restrict__ X, int ldx, const float* __restrict__
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   auto load_stage = [&](int c, int st) { ld.load(c, sbase + st * kStage * 4, kTcWPitch); };
 
-  float big[2][NB][4], small[2][NB][4];
+  float big[MTW][NB][4], small[MTW][NB][4];
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+  for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
@@ -460,8 +463,9 @@ sgemm_tcw_kernel(const float* __restrict__ X, int ldx, const float* __restrict__
     if (i < nch) load_stage(i, i);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  const int wc = (w & 3) * 32;                 // my 32 columns of the tile
-  const int k8lo = (w >> 2) * 16;              // my two k8 steps of each stage
+  const int kg = w / WPG, wi = w % WPG;
+  const int wc = wi * 32 * HV;                 // my columns of the tile
+  const int k8lo = kg * (kGemmKT / KG);        // my k8 steps of each stage
   for (int c = 0; c < nch; ++c) {
     const int st = c % STAGES;
     asm volatile("cp.async.wait_group %0;" ::"n"(STAGES - 2) : "memory");
@@ -472,20 +476,25 @@ sgemm_tcw_kernel(const float* __restrict__ X, int ldx, const float* __restrict__
     const float* ws_ = smem + st * kStage;
     const float* xs_ = ws_ + kWs;
 #pragma unroll
-    for (int kq = 0; kq < kGemmKT / 2; kq += 8) {
+    for (int kq = 0; kq < kGemmKT / KG; kq += 8) {
       const int k8 = k8lo + kq;
-      // A (weights): rows k8+t and k8+t+4, physical columns 4g .. 4g+3
-      const float4 wlo = *reinterpret_cast<const float4*>(ws_ + (k8 + t) * kTcWPitch + wc + 4 * g);
-      const float4 whi = *reinterpret_cast<const float4*>(ws_ + (k8 + t + 4) * kTcWPitch + wc + 4 * g);
-      uint32_t ah[2][4], al[2][4];
-      split_tf32(wlo.x, ah[0][0], al[0][0]);   // m-tile 0: (g, k t), (g+8, k t)
-      split_tf32(wlo.y, ah[0][1], al[0][1]);
-      split_tf32(wlo.z, ah[1][0], al[1][0]);   // m-tile 1
-      split_tf32(wlo.w, ah[1][1], al[1][1]);
-      split_tf32(whi.x, ah[0][2], al[0][2]);   // k t+4
-      split_tf32(whi.y, ah[0][3], al[0][3]);
-      split_tf32(whi.z, ah[1][2], al[1][2]);
-      split_tf32(whi.w, ah[1][3], al[1][3]);
+      // A (weights): rows k8+t and k8+t+4; per 32-column half, physical columns
+      // 4g .. 4g+3 = (m-tile 0: g, g+8; m-tile 1: g, g+8)
+      uint32_t ah[MTW][4], al[MTW][4];
+#pragma unroll
+      for (int hv = 0; hv < HV; ++hv) {
+        const float4 wlo = *reinterpret_cast<const float4*>(ws_ + (k8 + t) * kTcWPitch + wc + 32 * hv + 4 * g);
+        const float4 whi = *reinterpret_cast<const float4*>(ws_ + (k8 + t + 4) * kTcWPitch + wc + 32 * hv + 4 * g);
+        const int m0 = 2 * hv;
+        split_tf32(wlo.x, ah[m0][0], al[m0][0]);
+        split_tf32(wlo.y, ah[m0][1], al[m0][1]);
+        split_tf32(wlo.z, ah[m0 + 1][0], al[m0 + 1][0]);
+        split_tf32(wlo.w, ah[m0 + 1][1], al[m0 + 1][1]);
+        split_tf32(whi.x, ah[m0][2], al[m0][2]);
+        split_tf32(whi.y, ah[m0][3], al[m0][3]);
+        split_tf32(whi.z, ah[m0 + 1][2], al[m0 + 1][2]);
+        split_tf32(whi.w, ah[m0 + 1][3], al[m0 + 1][3]);
+      }
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb) {
         const float* xr = xs_ + (nb * 8 + g) * kTcXPitch + k8 + t;
@@ -493,7 +502,7 @@ sgemm_tcw_kernel(const float* __restrict__ X, int ldx, const float* __restrict__
         split_tf32(xr[0], bh0, bl0);
         split_tf32(xr[4], bh1, bl1);
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
+        for (int mt = 0; mt < MTW; ++mt) {
           mma_tf32(small[mt][nb], al[mt], bh0, bh1);
           mma_tf32(small[mt][nb], ah[mt], bl0, bl1);
           mma_tf32(big[mt][nb], ah[mt], bh0, bh1);
@@ -503,44 +512,45 @@ sgemm_tcw_kernel(const float* __restrict__ X, int ldx, const float* __restrict__
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+  for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
       for (int i = 0; i < 4; ++i) big[mt][nb][i] += small[mt][nb][i];
-  {                            // k-group 1 hands its sums to k-group 0 (fixed order)
+  {                            // k-groups 1.. hand their sums to k-group 0 (fixed order)
     __syncthreads();
-    float* red = smem;         // [4 warps][2][NB][4][32 lanes]
-    constexpr int per = 2 * NB * 4;
-    if (w >= 4) {
+    float* red = smem;         // [KG-1][WPG warps][MTW][NB][4][32 lanes]
+    constexpr int per = MTW * NB * 4;
+    if (kg > 0) {
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+      for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            red[(((w - 4) * per) + (mt * NB + nb) * 4 + i) * 32 + lane] = big[mt][nb][i];
+            red[((((kg - 1) * WPG + wi) * per) + (mt * NB + nb) * 4 + i) * 32 + lane] = big[mt][nb][i];
     }
     __syncthreads();
-    if (w < 4) {
+    if (kg == 0) {
+      for (int gg = 1; gg < KG; ++gg)
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
-        for (int nb = 0; nb < NB; ++nb)
+          for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            big[mt][nb][i] += red[((w * per) + (mt * NB + nb) * 4 + i) * 32 + lane];
+            for (int i = 0; i < 4; ++i)
+              big[mt][nb][i] += red[((((gg - 1) * WPG + wi) * per) + (mt * NB + nb) * 4 + i) * 32 + lane];
     }
   }
   const size_t tile_elems = (size_t)M * kGemmTileN;
   float* part = ws + ((size_t)tile * ksplit + ks) * tile_elems;
-  if (w < 4) {
+  if (kg == 0) {
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb) {
         // C: (m = g, seq 2t / 2t+1) and (m = g + 8, seq 2t / 2t+1)
-        const int col0 = wc + 4 * g + 2 * mt, col1 = col0 + 1;
+        const int col0 = wc + 32 * (mt >> 1) + 4 * g + 2 * (mt & 1), col1 = col0 + 1;
         const int s0 = nb * 8 + 2 * t, s1 = s0 + 1;
         if (s0 < M) {
           part[(size_t)s0 * kGemmTileN + col0] = big[mt][nb][0];
@@ -575,16 +585,16 @@ sgemm_tcw_kernel(const float* __restrict__ X, int ldx, const float* __restrict__
   if (tid == 0 && ksplit > 1) tickets[tile] = 0;
 }
 
-template <int NB, int STAGES>
+template <int NB, int STAGES, int KG = 2>
 int launch_sgemm_tcw(const float* X, int ldx, const float* W, int ldw, float* Y, int ldy,
                      const float* R, int ldr, int M, int N, int K, int ksplit, int epilogue,
                      float* ws, int32_t* tickets, cudaStream_t s) {
   const int tiles = (N + kGemmTileN - 1) / kGemmTileN;
   const size_t smem =
       (size_t)STAGES * (kGemmKT * kTcWPitch + 8 * NB * kTcXPitch) * sizeof(float);
-  IG_CUDA_STATUS(cudaFuncSetAttribute(sgemm_tcw_kernel<NB, STAGES>,
+  IG_CUDA_STATUS(cudaFuncSetAttribute(sgemm_tcw_kernel<NB, STAGES, KG>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  sgemm_tcw_kernel<NB, STAGES><<<dim3(tiles, ksplit), kGemmWarps * 32, smem, s>>>(
+  sgemm_tcw_kernel<NB, STAGES, KG><<<dim3(tiles, ksplit), kGemmWarps * 32, smem, s>>>(
       X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, ws, tickets);
   IG_LAUNCH_STATUS();
   return IG_OK;
@@ -685,10 +695,6 @@ extern "C" int ig_sgemm_tc(const float* X, int ldx, const float* W, int ldw, flo
     const char* v = getenv("IG_TC_VARIANT");
     return v ? atoi(v) : 4;
   }();
-  if (variant == 5 && M > 8 && M <= 16)     // sweep: 4 stages, 2 CTAs/SM
-    return launch_sgemm_tcw<2, 4>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
-  if (variant == 6 && M > 8 && M <= 16)     // sweep: 5 stages, 2 CTAs/SM
-    return launch_sgemm_tcw<2, 5>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);
   if (variant == 4 || variant >= 5) {
     if (M <= 8)
       return launch_sgemm_tcw<1, 3>(X, ldx, W, ldw, Y, ldy, R, ldr, M, N, K, ksplit, epilogue, workspace, tickets, s);

@@ -137,6 +137,9 @@ def _simulate_prefill_rows(n: int, limit: int | None, policy: EvictionPolicy):
     return row_of, arrival, lastf, ctr, overwrites
 
 
+_LAYER_POS = object()     # _attend default: the layer's ig_append positions
+
+
 class DecodeEngine:
     """Batched InfiniGen decode on one GPU (or one head shard of a TP group).
 
@@ -170,13 +173,17 @@ class DecodeEngine:
         -> select -> resident plan) on its own high-priority stream, overlapping
         layer l's append/attention/W_O/FFN (traces recorded with scores use the
         compute stream).
+    append_stream : without a pool limit, run ig_append beside the attention on
+        its own stream (the attention takes the append position from st.s_len).
+        Measured neutral at C3 (803.9 vs 803.8 tok/s), so off by default.
     """
 
     def __init__(self, model, config: RunConfig, *, max_steps: int | None = None,
                  pool_dtype: str = "f16", device=None, group=None, fetch_ctas: int = 32,
                  fetch_threads: int = 32, fetch_priority: int = 0, hbm_layers: int = 0,
                  fetch_impl: str = "tma", fetch_rows: int = 16, dense: str = "tc",
-                 cuda_graph: bool = False, resident: bool = False, spec_stream: bool = True):
+                 cuda_graph: bool = False, resident: bool = False, spec_stream: bool = True,
+                 append_stream: bool = False):
         config.validate()
         _lib.load()
         _enable_ieee_fp32()
@@ -235,6 +242,7 @@ class DecodeEngine:
         self.resident = bool(resident)
         self._res_valid = False
         self.spec_stream_on = bool(spec_stream)
+        self.append_stream_on = bool(append_stream)
         self.scale = float(np.float32(1.0 / np.sqrt(d)))   # speculation.py:127
         self._load_weights(model)
         self._alloc()
@@ -332,7 +340,10 @@ class DecodeEngine:
         self.compute = torch.cuda.Stream(device=dev)
         self.fetch_stream = torch.cuda.Stream(device=dev, priority=self.fetch_priority)
         self.spec_stream = torch.cuda.Stream(device=dev, priority=-1)
+        self.append_stream = torch.cuda.Stream(device=dev)
         self.ev_q = [torch.cuda.Event() for _ in range(L)]
+        self.ev_qkv = [torch.cuda.Event() for _ in range(L)]
+        self.ev_app = [torch.cuda.Event() for _ in range(L)]
         self.ev_sel = [torch.cuda.Event() for _ in range(L)]
         self.ev_fetch = [torch.cuda.Event() for _ in range(L)]
         self.ev_att = [torch.cuda.Event() for _ in range(L)]
@@ -751,22 +762,24 @@ class DecodeEngine:
                   self.fetch_ctas, max(1, self.fetch_threads // 32), self.fetch_rows,
                   self.fetch_stream.cuda_stream)
 
-    def _attend(self, li: int, stage, idx, n, stage_rows: int, cs: int) -> None:
+    def _attend(self, li: int, stage, idx, n, stage_rows: int, cs: int, pos=_LAYER_POS) -> None:
         Hgd = self.Hg * self.d
         q, ld = self.qkv, self.qkvq.stride(0)
         _lib.call("ig_attend", q.data_ptr(), ld, q.data_ptr() + 4 * Hgd,
                   q.data_ptr() + 8 * Hgd, ld, stage.data_ptr(), _lib.ELT[self.elt],
-                  _lib.ptr(idx), _lib.ptr(n), self.pos[li].data_ptr(), self.st.data_ptr(),
+                  _lib.ptr(idx), _lib.ptr(n), _lib.ptr(self.pos[li] if pos is _LAYER_POS else pos),
+                  self.st.data_ptr(),
                   self.B, self.Hg, self.d, stage_rows, self.att_partial.data_ptr(),
                   self.att_tickets.data_ptr(), self.attn.data_ptr(), Hgd, cs)
 
-    def _attend_slots(self, li: int, cs: int) -> None:
+    def _attend_slots(self, li: int, cs: int, pos=_LAYER_POS) -> None:
         Hgd = self.Hg * self.d
         q, ld = self.qkv, self.qkvq.stride(0)
         _lib.call("ig_attend_slots", q.data_ptr(), ld, q.data_ptr() + 4 * Hgd,
                   q.data_ptr() + 8 * Hgd, ld, self.stage_res[li - 1].data_ptr(),
                   _lib.ELT[self.elt], self.slot_id[li - 1].data_ptr(),
-                  self.slot_used[li - 1].data_ptr(), self.pos[li].data_ptr(), self.st.data_ptr(),
+                  self.slot_used[li - 1].data_ptr(),
+                  _lib.ptr(self.pos[li] if pos is _LAYER_POS else pos), self.st.data_ptr(),
                   self.B, self.Hg, self.d, self.cap, self.att_partial.data_ptr(),
                   self.att_tickets.data_ptr(), self.attn.data_ptr(), Hgd, cs)
 
@@ -827,6 +840,11 @@ class DecodeEngine:
         s = self.s_host
         graph = self._graph_mode
         recording = (cfg.record_selection or cfg.record_scores) and not graph
+        # append stream: without a pool limit the append position is st.s_len, so the
+        # attention does not wait for ig_append, which then runs beside it
+        AP = (self.append_stream if (self.append_stream_on and cfg.pool_limit is None and not recording)
+              else C)
+        aps = AP.cuda_stream
         recs = [[None] * L for _ in range(B)]
         spec_scores = [None] * L
         C.wait_stream(torch.cuda.current_stream(self.device))
@@ -863,6 +881,8 @@ class DecodeEngine:
                 if speculative and li >= 1 and SP is not C:
                     # spec(li) done: qspec is free for the fused GEMM, idx/n/plan of li ready
                     C.wait_event(self.ev_sel[li])
+                if li >= 1 and AP is not C:
+                    C.wait_event(self.ev_app[li - 1])   # append(li-1) read qkv: free it
                 nxt = li + 1
                 if nxt < L:
                     if speculative:
@@ -936,6 +956,9 @@ class DecodeEngine:
                     self._gemm(self.x_a, self.wqkv[li], self.qkv, cs)
                 sel = speculative and li >= 1
                 ldq = self.qkvq.stride(0)
+                if AP is not C:
+                    self.ev_qkv[li].record(C)
+                    AP.wait_event(self.ev_qkv[li])
                 _lib.call("ig_append", self.qkv.data_ptr() + 4 * Hgd, self.qkv.data_ptr() + 8 * Hgd,
                           ldq, self._pool_layer_dev(li), _lib.ELT[self.elt],
                           _lib.ptr(self.pk[li - 1]) if sel else None,
@@ -945,23 +968,26 @@ class DecodeEngine:
                           2 if sel else 1, _lib.ptr(self.idx[li]) if sel else None,
                           _lib.ptr(self.n[li]) if sel else None, self.cap,
                           self.st.data_ptr(), B, Hg, d, self.S_max, self.pos[li].data_ptr(),
-                          self.events[li].data_ptr(), cs)
+                          self.events[li].data_ptr(), aps)
                 if resident and li == 0:            # keep layer 0's mirror complete
                     _lib.call("ig_stage_put", self.qkv.data_ptr() + 4 * Hgd,
                               self.qkv.data_ptr() + 8 * Hgd, ldq, self.pos[0].data_ptr(),
                               self.stage_full[0].data_ptr(), _lib.ELT[self.elt], B, Hg, d,
-                              self.S_max, cs)
+                              self.S_max, aps)
+                if AP is not C:
+                    self.ev_app[li].record(AP)
+                apos = None if AP is not C else self.pos[li]   # NULL: pos = st.s_len
                 C.wait_event(self.ev_fetch[li])
                 self._mark("attend", li, C, True)
                 if sel and resident:
-                    self._attend_slots(li, cs)
+                    self._attend_slots(li, cs, apos)
                 elif sel:
-                    self._attend(li, self.stage_sel[li % 2], self.idx[li], self.n[li], self.cap, cs)
+                    self._attend(li, self.stage_sel[li % 2], self.idx[li], self.n[li], self.cap, cs, apos)
                 elif li < self.hbm_layers:
-                    self._attend(li, self.pool_hbm[li], None, None, self.S_max, cs)
+                    self._attend(li, self.pool_hbm[li], None, None, self.S_max, cs, apos)
                 else:
                     stage = self.stage_full[0] if speculative else self.stage_full[li % 2]
-                    self._attend(li, stage, None, None, self.S_max, cs)
+                    self._attend(li, stage, None, None, self.S_max, cs, apos)
                 self._mark("attend", li, C, False)
                 self.ev_att[li].record(C)
                 if self.world > 1:
@@ -978,6 +1004,8 @@ class DecodeEngine:
                 if recording:
                     self._record(li, s, recs, spec_scores)
                 x = x_new
+            if AP is not C:
+                C.wait_event(self.ev_app[L - 1])    # every append read this step's state
             _lib.call("ig_step_advance", self.st.data_ptr(), cs)
             inst = self._inst
             if inst is not None and not graph and inst["k"] < inst["steps"]:
@@ -996,6 +1024,8 @@ class DecodeEngine:
             elif not self.hbm_layers and not resident:
                 last0 = 0 if speculative else (L - 1 if (L - 1) % 2 == 0 else L - 2)
                 Fs.wait_event(self.ev_att[last0])
+                if AP is not C:
+                    Fs.wait_event(self.ev_app[0])   # this step's layer-0 row is in the pool
                 self._issue_full_fetch(0, s_next, self.stage_full[0])
                 self.ev_fetch[0].record(Fs)
                 self._prefetched0 = True
