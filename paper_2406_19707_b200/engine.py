@@ -162,7 +162,8 @@ class DecodeEngine:
         keep layer 0's rows -- which every step reads in full (engine.py:393-396)
         -- resident in HBM, so they never cross the host link.  Traces keep the
         reference byte accounting; bench.py reports moved bytes separately.
-    resident : keep each speculative layer's fetched set in HBM across steps
+    resident : (default: on for the speculative scheme without hbm_layers)
+        keep each speculative layer's fetched set in HBM across steps
         (a slot table of at most `cap` rows per (layer, seq, head)) and fetch
         only the rows that enter the selection; layer 0's rows are mirrored in
         HBM and the appended row is written to the mirror in the same step.
@@ -182,7 +183,7 @@ class DecodeEngine:
                  pool_dtype: str = "f16", device=None, group=None, fetch_ctas: int = 32,
                  fetch_threads: int = 32, fetch_priority: int = 0, hbm_layers: int = 0,
                  fetch_impl: str = "tma", fetch_rows: int = 16, dense: str = "tc",
-                 cuda_graph: bool = False, resident: bool = False, spec_stream: bool = True,
+                 cuda_graph: bool = False, resident: bool | None = None, spec_stream: bool = True,
                  append_stream: bool = False):
         config.validate()
         _lib.load()
@@ -237,6 +238,8 @@ class DecodeEngine:
         if hbm_layers not in (0, 1) or hbm_layers > spec.layers:
             raise ValueError("hbm_layers must be 0 or 1")
         self.hbm_layers = hbm_layers
+        if resident is None:
+            resident = scheme == "speculative" and not hbm_layers
         if resident and (scheme != "speculative" or hbm_layers):
             raise ValueError("resident needs the speculative scheme and hbm_layers=0")
         self.resident = bool(resident)
@@ -413,6 +416,8 @@ class DecodeEngine:
         """Move layer 0's rows between the host pool and the HBM tier."""
         if n not in (0, 1):
             raise ValueError("hbm_layers must be 0 or 1")
+        if n == 1 and self.resident:
+            raise ValueError("hbm_layers=1 needs resident=False (resident mode mirrors layer 0)")
         torch.cuda.synchronize(self.device)
         if n == self.hbm_layers:
             return

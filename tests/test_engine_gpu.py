@@ -91,7 +91,10 @@ def test_engine_f32_pool_matches_oracle(mname, rname):
     ocfg = run_config(rname, record_selection=True)
     model = sk if ocfg.scheme == "speculative" else plain
     sessions = oracle_sessions(model, ocfg)
-    eng = DecodeEngine.from_sessions(model, engine_cfg(ocfg), copy.deepcopy(sessions), pool_dtype="f32")
+    # resident=False: the reference's data movement (refetch every step); the resident
+    # default has the same bars in tests/test_resident_gpu.py
+    eng = DecodeEngine.from_sessions(model, engine_cfg(ocfg), copy.deepcopy(sessions), pool_dtype="f32",
+                                     resident=False)
     try:
         ref_out, ref_recs = oracle_decode(sessions, ocfg.gen_len)
         got = [eng.x.cpu().numpy()]
@@ -284,7 +287,7 @@ def test_hbm_resident_layer0_is_identical(rname):
     outs, recs, rows = [], [], []
     for hbm in (0, 1):
         eng = DecodeEngine.from_sessions(model, engine_cfg(ocfg), copy.deepcopy(sessions),
-                                         pool_dtype="f32", hbm_layers=hbm)
+                                         pool_dtype="f32", hbm_layers=hbm, resident=False)
         try:
             outs.append(np.stack([eng.decode_step().cpu().numpy() for _ in range(ocfg.gen_len)]))
             recs.append(eng.records)
@@ -325,7 +328,7 @@ def test_fetch_implementations_identical(impl, ctas, threads, rows):
     outs = []
     for kw in ({}, dict(fetch_impl=impl, fetch_ctas=ctas, fetch_threads=threads, fetch_rows=rows)):
         eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg), copy.deepcopy(sessions),
-                                         pool_dtype="f16", **kw)
+                                         pool_dtype="f16", resident=False, **kw)
         try:
             outs.append(np.stack([eng.decode_step().cpu().numpy() for _ in range(ocfg.gen_len)]))
         finally:
@@ -382,7 +385,8 @@ def test_long_run_eviction_and_saturation(policy):
     ocfg = O.RunConfig(scheme="speculative", prompt_len=24, gen_len=300, batch=1,
                        pool_limit=20, pool_policy=O.Policy(policy), record_selection=True)
     sessions = oracle_sessions(sk, ocfg)
-    eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg), copy.deepcopy(sessions), pool_dtype="f32")
+    eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg), copy.deepcopy(sessions), pool_dtype="f32",
+                                     resident=False)
     try:
         ref_out, ref_recs = oracle_decode(sessions, ocfg.gen_len)
         got = np.stack([eng.x.cpu().numpy()] + [eng.decode_step().cpu().numpy()
@@ -505,7 +509,8 @@ def test_cuda_graph_replay_is_identical(rname, pool):
     outs, meta = [], []
     for graph in (False, True):
         eng = DecodeEngine.from_sessions(model, engine_cfg(ocfg, record_selection=False),
-                                         copy.deepcopy(sessions), pool_dtype=pool, cuda_graph=graph)
+                                         copy.deepcopy(sessions), pool_dtype=pool, cuda_graph=graph,
+                                         resident=False)
         try:
             outs.append(np.stack([eng.decode_step().cpu().numpy() for _ in range(ocfg.gen_len)]))
             meta.append((eng.counter.cpu().numpy(), eng.lastf.cpu().numpy(), eng.s_host, eng.iteration))
