@@ -208,7 +208,7 @@ def _config(a) -> dict:
             "outlier_scale": WORKLOAD["outlier_scale"], "kv_pool": "pinned host, f16",
             "fetch": (f"{a.fetch_impl} x {a.fetch_ctas} CTAs x {a.fetch_threads} threads"
                       + (f" x {a.fetch_rows} rows/batch" if a.fetch_impl == "tma" else "")),
-            "parallelism": f"tp{a.gpus} (heads)" if a.gpus > 1 else "single GPU",
+            "parallelism": f"tp{a.gpus} (attention heads + FFN columns)" if a.gpus > 1 else "single GPU",
             "dense": {"ig": "ig_sgemm_rows (f32 CUDA cores)", "tc": "ig_sgemm_tc (3xTF32 tensor cores)",
                       "cublas": "cuBLAS f32 (TF32 off)"}[a.dense],
             "cuda_graph": bool(a.cuda_graph), "resident": bool(a.resident),

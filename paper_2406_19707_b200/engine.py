@@ -203,6 +203,12 @@ class DecodeEngine:
         self.H, self.D, self.d, self.L, self.F = H, D, d, L, spec.ffn_dim
         self.Hg = H // self.world
         self.h0 = self.rank * self.Hg
+        # FFN tensor parallelism (Megatron MLP: FFN-in column-parallel, FFN-out
+        # row-parallel, one all-reduce), so every rank streams 1/G of all weights;
+        # replicated if the hidden width does not split into 16-B multiples
+        F = spec.ffn_dim
+        self.Fg = F // self.world if (F % self.world == 0 and (F // self.world) % 4 == 0) else F
+        self.f0 = self.rank * self.Fg if self.Fg != F else 0
         self.B = config.batch
         self.elt = pool_dtype
         self.row_bytes = 2 * d * _lib.ELT_BYTES[pool_dtype]
@@ -278,8 +284,9 @@ class DecodeEngine:
             self.wfused.append(wf if len(parts) == 4 else None)
             self.wqkv.append(wf[:, :3 * (c1 - c0)])
             self.wo.append(_f32(lw.w_o, dev)[c0:c1].contiguous())
-            self.ffn_in.append(_f32(lw.ffn_in, dev))
-            self.ffn_out.append(_f32(lw.ffn_out, dev))
+            f0, f1 = self.f0, self.f0 + self.Fg
+            self.ffn_in.append(_f32(lw.ffn_in, dev)[:, f0:f1].contiguous())
+            self.ffn_out.append(_f32(lw.ffn_out, dev)[f0:f1].contiguous())
             self.ln.append(tuple(_f32(getattr(lw, f), dev) for f in
                                  ("ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias")))
 
@@ -309,7 +316,7 @@ class DecodeEngine:
         self.qspec = self.qkvq[:, 3 * Hg * d:]
         self.attn = torch.empty((B, Hg * d), dtype=f32, device=dev)
         self.o = torch.empty((B, D), dtype=f32, device=dev)
-        self.hidden = torch.empty((B, F), dtype=f32, device=dev)
+        self.hidden = torch.empty((B, self.Fg), dtype=f32, device=dev)
         self.scores = torch.empty((B, Hg, S), dtype=f32, device=dev)
         self.maxkey = torch.zeros((B, Hg), dtype=i32, device=dev)      # rehearse scratch
         self.rtickets = torch.zeros((B, Hg), dtype=i32, device=dev)    # (left zeroed)
@@ -327,7 +334,8 @@ class DecodeEngine:
         if self.resident:
             self._alloc_resident()
         # skinny-GEMM workspace: the largest ceil(N/128) * ksplit * B * 128 over the projections
-        shapes = [(4 * Hg * d, D), (3 * Hg * d, D), (Hg * d, D), (D, Hg * d), (F, D), (D, F)]   # (N, K)
+        Fg = self.Fg
+        shapes = [(4 * Hg * d, D), (3 * Hg * d, D), (Hg * d, D), (D, Hg * d), (Fg, D), (D, Fg)]   # (N, K)
         ws = 0
         self.gemm_ksplit = {}
         for N_, K_ in shapes:
@@ -565,7 +573,10 @@ class DecodeEngine:
                         dist.all_reduce(o, group=self.group)
                     mid = x + o
                     xf = layernorm(mid, g2, b2, spec.ln_eps)
-                    x = mid + torch.relu(xf @ self.ffn_in[li]) @ self.ffn_out[li]
+                    ffn = torch.relu(xf @ self.ffn_in[li]) @ self.ffn_out[li]
+                    if self.Fg != self.F:
+                        dist.all_reduce(ffn, group=self.group)   # row-parallel FFN-out
+                    x = mid + ffn
                     # pool rows (keep_tok: which prompt token survives in each row)
                     kvrows = torch.stack([k[:, keep], v[:, keep]], dim=2).to(T).contiguous()
                     base = self._pool_layer_host(li) + b * Hg * S * self.row_bytes
@@ -720,7 +731,7 @@ class DecodeEngine:
         rows = [("rehearse_count", rehearse, 4 * B * Hg * s * (kc + 1)),
                 ("select", select, 4 * B * Hg * s),
                 ("attend", attend, n_tot * Hg * self.row_bytes),
-                ("dense_ffn_in", ffn_in, 4 * (self.D * self.F + B * self.D + B * self.F))]
+                ("dense_ffn_in", ffn_in, 4 * (self.D * self.Fg + B * self.D + B * self.Fg))]
         out = {}
         for name, fn, nbytes in rows:
             ms = best(fn)
@@ -1005,7 +1016,12 @@ class DecodeEngine:
                           float(spec.ln_eps), B, self.D, self.x_f.data_ptr(), cs)
                 self._gemm(self.x_f, self.ffn_in[li], self.hidden, cs, epilogue=1)
                 x_new = self.xbuf[1] if x is self.xbuf[0] else self.xbuf[0]
-                self._gemm(self.hidden, self.ffn_out[li], x_new, cs, epilogue=2, R=self.o)
+                if self.Fg != self.F:               # row-parallel FFN-out: sum the ranks
+                    self._gemm(self.hidden, self.ffn_out[li], x_new, cs)
+                    dist.all_reduce(x_new, group=self.group)
+                    x_new.add_(self.o)
+                else:
+                    self._gemm(self.hidden, self.ffn_out[li], x_new, cs, epilogue=2, R=self.o)
                 if recording:
                     self._record(li, s, recs, spec_scores)
                 x = x_new
