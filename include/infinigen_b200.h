@@ -237,6 +237,20 @@ int ig_sgemm_tc(const float* X, int ldx, const float* W, int ldw, float* Y, int 
                 const float* R, int ldr, int M, int N, int K, int ksplit, int epilogue,
                 float* workspace, size_t workspace_floats, int32_t* tickets, void* stream);
 
+/* Same contract and 3xTF32 arithmetic over weights PACKED once at load time
+ * (ig_sgemm_pack: 16-KB blocks of 32 rows x 128 columns in MMA-fragment
+ * order, contiguous in (column tile, row block) order -- the whole GEMM is one
+ * sequential stream).  Persistent stream-K grid (no ksplit argument):
+ * ig_sgemm_packed_sizes gives the packed buffer (floats), the workspace
+ * (floats) and ticket (ints, zeroed once, left zeroed) sizes for (M, N, K).
+ * X 16-B aligned, ldx and K multiples of 4.  Deterministic on a given device. */
+int ig_sgemm_packed_sizes(int M, int N, int K, size_t* packed_floats, size_t* workspace_floats,
+                          size_t* tickets);
+int ig_sgemm_pack(const float* W, int ldw, int N, int K, float* packed, void* stream);
+int ig_sgemm_packed(const float* X, int ldx, const float* packed, int N, int K, float* Y, int ldy,
+                    const float* R, int ldr, int M, int epilogue, float* workspace,
+                    size_t workspace_floats, int32_t* tickets, size_t ntickets, void* stream);
+
 /* ---- step bookkeeping -------------------------------------------------- */
 /* s_len = min(s_len + 1, limit), seq += 2, step += 1 (engine.py:377-378). */
 int ig_step_advance(ig_step_state* st, void* stream);

@@ -57,6 +57,10 @@ _SIGS = {
     "ig_sgemm_rows": [_P, _I, _P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _I, _P, _SZ, _P, _P],
     "ig_sgemm_tc_ksplit": [_I, _I, _I],
     "ig_sgemm_tc": [_P, _I, _P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _I, _P, _SZ, _P, _P],
+    "ig_sgemm_packed_sizes": [_I, _I, _I, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ),
+                              ctypes.POINTER(_SZ)],
+    "ig_sgemm_pack": [_P, _I, _I, _I, _P, _P],
+    "ig_sgemm_packed": [_P, _I, _P, _I, _I, _P, _I, _P, _I, _I, _I, _P, _SZ, _P, _SZ, _P],
     "ig_step_advance": [_P, _P],
     "ig_layernorm": [_P, _P, _P, _F, _I, _I, _P, _P],
 }

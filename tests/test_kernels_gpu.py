@@ -259,6 +259,49 @@ def test_sgemm_rows_vs_float64(M, N, K, epilogue, fn):
     assert not tk.any()
 
 
+@pytest.mark.parametrize("M,N,K", [(1, 128, 64), (5, 260, 100), (8, 512, 5120), (16, 5120, 5120),
+                                   (17, 1024, 2048), (32, 384, 4096), (16, 20480, 512),
+                                   (16, 20480, 5120), (4, 4096, 11008), (12, 200, 36)])
+@pytest.mark.parametrize("epilogue", [0, 1, 2])
+def test_sgemm_packed_vs_float64(M, N, K, epilogue):
+    """ig_sgemm_pack + ig_sgemm_packed (persistent stream-K 3xTF32 over packed
+    weights) vs float64: every M template, ragged column tiles and row blocks,
+    tile segments split over several CTAs, fused epilogues, strided X/Y;
+    bit-identical on repeat; tickets left zeroed."""
+    import ctypes
+    import torch
+    from paper_2406_19707_b200 import _lib
+    g = torch.Generator(device="cuda")
+    g.manual_seed(M * 1000 + N + K + 7)
+    X = torch.randn(M, K + 4, device="cuda", generator=g)[:, :K]        # ldx > K
+    W = torch.randn(K, N + 8, device="cuda", generator=g)[:, :N]        # ld > N
+    R = torch.randn(M, N, device="cuda", generator=g)
+    pf, wf, tf = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+    _lib.call("ig_sgemm_packed_sizes", M, N, K, ctypes.byref(pf), ctypes.byref(wf), ctypes.byref(tf),
+              kernels=0)
+    P = torch.full((pf.value,), float("nan"), device="cuda")
+    _lib.call("ig_sgemm_pack", W.data_ptr(), W.stride(0), N, K, P.data_ptr(), _lib.stream_handle())
+    ws = torch.empty(wf.value, device="cuda")
+    tk = torch.zeros(tf.value, dtype=torch.int32, device="cuda")
+    outs = []
+    for _ in range(2):
+        Yb = torch.full((M, N + 3), float("nan"), device="cuda")
+        Y = Yb[:, :N]
+        _lib.call("ig_sgemm_packed", X.data_ptr(), X.stride(0), P.data_ptr(), N, K, Y.data_ptr(),
+                  Yb.stride(0), R.data_ptr() if epilogue == 2 else None, N if epilogue == 2 else 0, M,
+                  epilogue, ws.data_ptr(), ws.numel(), tk.data_ptr(), tk.numel(), _lib.stream_handle())
+        outs.append(Y.clone())
+        assert torch.isnan(Yb[:, N:]).all()                 # nothing written past N
+    ref = X.double() @ W.double()
+    if epilogue == 1:
+        ref = ref.clamp_min(0)
+    elif epilogue == 2:
+        ref = ref + R.double()
+    torch.testing.assert_close(outs[0].double(), ref, rtol=1e-5, atol=2e-4 * max(1.0, K ** 0.5 / 8))
+    assert torch.equal(outs[0], outs[1])
+    assert not tk.any()
+
+
 @pytest.mark.parametrize("elt", ["f16", "bf16"])
 def test_attend_512b_row_variants_match(elt):
     """The three 512-B-row attention kernels -- tensor cores (default), register-fed
