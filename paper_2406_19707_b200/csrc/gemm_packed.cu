@@ -43,12 +43,12 @@ namespace ig {
 namespace packed {
 
 constexpr int kTileN = 128;            // output columns per tile
-constexpr int kChunkK = 32;            // weight rows per block
-constexpr int kBlockFloats = kTileN * kChunkK;   // 4096 floats = 16 KB
+constexpr int kChunkK = 64;            // weight rows per block
+constexpr int kBlockFloats = kTileN * kChunkK;   // 8192 floats = 32 KB
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = kConsumerWarps * 32;
-// (CTAs per SM, ring stages): M <= 16 runs 2 x 6 (96-KB rings) or 3 x 4;
-// M <= 32 (64 accumulator registers per lane) 1 x 12.  Registers: an SM
+// (CTAs per SM, ring stages): M <= 16 runs 2 x 3 (96-KB rings); M <= 32 (64
+// accumulator registers per lane) 1 x 6.  Registers: an SM
 // sub-partition holds 16K, i.e. 2 CTAs x 8 warps -> 128 per thread, 3 -> 80.
 template <int CPS> struct RegCap { static constexpr int v = CPS == 1 ? 255 : (CPS == 2 ? 128 : 80); };
 
@@ -135,17 +135,16 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
   // Thread 0 keeps the ring full: chunks g0 .. g0 + S - 1 now, then at
   // iteration j the stage released at iteration j - 1 gets chunk j - 1 + S
   // (one iteration of slack, so the wait on `empty` rarely blocks).
-  auto issue = [&](int jj) {
-    const int st = jj % kStages;
+  auto issue = [&](int jj, int st) {
     bar_expect_tx(full_s + 8 * st, kBlockFloats * 4);
     bulk_g2s(ring_s + st * kBlockFloats * 4, P + (size_t)(g0 + jj) * kBlockFloats,
              kBlockFloats * 4, full_s + 8 * st);
   };
   if (tid == 0)
-    for (int jj = 0; jj < kStages && g0 + jj < g1; ++jj) issue(jj);
+    for (int jj = 0; jj < kStages && g0 + jj < g1; ++jj) issue(jj, jj);
 
-  // ---- consumer warps: kg = k-group (k8 steps 2 kg, 2 kg + 1 of a block),
-  // wi = 32-column slab of the tile
+  // ---- kg = k-group (k16 steps 2 kg, 2 kg + 1 of a block), wi = 32-column
+  // slab of the tile
   const int g = lane >> 2, t = lane & 3;
   const int kg = w >> 2, wi = w & 3;
   float big[MTW][NB][4], small[MTW][NB][4];
@@ -156,61 +155,75 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
 #pragma unroll
       for (int e = 0; e < 4; ++e) big[mt][nb][e] = small[mt][nb][e] = 0.f;
 
-  // x fragments of block i: rows m = 8 nb + g, k = 32 kc + 16 kg + 4 t + e
-  // (e = 2 s + h: k8 step s, MMA k column t + 4 h)
-  auto load_x = [&](int i, float (&xv)[NB][4]) {
-    const int k = (i % C) * kChunkK + 16 * kg + 4 * t;
+  // x fragments of a block at row kc: rows m = 8 nb + g,
+  // k = 64 kc + 32 kg + 16 s + 4 t + (0..3) for k16 step s
+  const float* xrow[NB];
+  bool mok[NB];
 #pragma unroll
-    for (int nb = 0; nb < NB; ++nb) {
-      const int m = 8 * nb + g;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (m < M && k < K && i < g1) v = __ldg(reinterpret_cast<const float4*>(X + (size_t)m * ldx + k));
-      xv[nb][0] = v.x; xv[nb][1] = v.y; xv[nb][2] = v.z; xv[nb][3] = v.w;
-    }
+  for (int nb = 0; nb < NB; ++nb) {
+    mok[nb] = 8 * nb + g < M;
+    xrow[nb] = X + (size_t)(mok[nb] ? 8 * nb + g : 0) * ldx + 32 * kg + 4 * t;
+  }
+  auto load_x = [&](int kc, bool ok, float4 (&xv)[NB][2]) {
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2) {
+        const int k = kc * kChunkK + 32 * kg + 16 * s2 + 4 * t;
+        xv[nb][s2] = (ok && mok[nb] && k < K)
+                         ? __ldg(reinterpret_cast<const float4*>(xrow[nb] + kc * kChunkK + 16 * s2))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
   };
-  float xa[NB][4], xb[NB][4], xc[NB][4];
-  load_x(g0, xa);
-  load_x(g0 + 1, xb);
+  float4 xa[NB][2], xb[NB][2];
+  int kc = g0 % C, tile = g0 / C;          // chunk g0 + j = (tile, kc)
+  int kcn = kc + 1 == C ? 0 : kc + 1;      // row block of the next chunk
+  load_x(kc, true, xa);
+  int st = 0, ph = 0;                      // ring stage and its phase parity
 
-  for (int i = g0; i < g1; ++i) {
-    const int j = i - g0, st = j % kStages;
-    load_x(i + 2, xc);
+  for (int j = 0, i = g0; i < g1; ++i, ++j) {
+    load_x(kcn, i + 1 < g1, xb);
     if (tid == 0 && j >= 1 && i - 1 + kStages < g1) {
-      bar_wait(empty_s + 8 * ((j - 1) % kStages), ((j - 1) / kStages) & 1);
-      issue(j - 1 + kStages);
+      const int sp = st == 0 ? kStages - 1 : st - 1;        // stage of iteration j - 1
+      bar_wait(empty_s + 8 * sp, (sp == kStages - 1 ? ph ^ 1 : ph));
+      issue(j - 1 + kStages, sp);
     }
-    bar_wait(full_s + 8 * st, (j / kStages) & 1);
-    const float* blk = ring + st * kBlockFloats;
-    // one k16 step per k-group: A fragments (hi, lo) of both m16 tiles
-    uint4 a[MTW][2];
+    bar_wait(full_s + 8 * st, ph);
+    const uint4* blk = reinterpret_cast<const uint4*>(ring + st * kBlockFloats);
 #pragma unroll
-    for (int mt = 0; mt < MTW; ++mt)
+    for (int s2 = 0; s2 < 2; ++s2) {
+      const int k16 = 2 * kg + s2;
+      uint4 a[MTW][2];
 #pragma unroll
-      for (int pt = 0; pt < 2; ++pt)
-        a[mt][pt] = reinterpret_cast<const uint4*>(blk)[(((kg * 4 + wi) * 2 + mt) * 2 + pt) * 32 + lane];
+      for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
-    for (int nb = 0; nb < NB; ++nb) {
-      uint32_t bh0, bl0, bh1, bl1;
-      split_h2(xa[nb][0], xa[nb][1], bh0, bl0);
-      split_h2(xa[nb][2], xa[nb][3], bh1, bl1);
+        for (int pt = 0; pt < 2; ++pt) a[mt][pt] = blk[(((k16 * 4 + wi) * 2 + mt) * 2 + pt) * 32 + lane];
 #pragma unroll
-      for (int mt = 0; mt < MTW; ++mt) {
-        mma_h(small[mt][nb], a[mt][1], bh0, bh1);
-        mma_h(small[mt][nb], a[mt][0], bl0, bl1);
-        mma_h(big[mt][nb], a[mt][0], bh0, bh1);
+      for (int nb = 0; nb < NB; ++nb) {
+        uint32_t bh0, bl0, bh1, bl1;
+        split_h2(xa[nb][s2].x, xa[nb][s2].y, bh0, bl0);
+        split_h2(xa[nb][s2].z, xa[nb][s2].w, bh1, bl1);
+#pragma unroll
+        for (int mt = 0; mt < MTW; ++mt) {
+          mma_h(small[mt][nb], a[mt][1], bh0, bh1);
+          mma_h(small[mt][nb], a[mt][0], bl0, bl1);
+          mma_h(big[mt][nb], a[mt][0], bh0, bh1);
+        }
       }
     }
     __syncwarp();
     if (lane == 0) bar_arrive(empty_s + 8 * st);
+    if (++st == kStages) { st = 0; ph ^= 1; }
 #pragma unroll
-    for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) { xa[nb][e] = xb[nb][e]; xb[nb][e] = xc[nb][e]; }
-
-    if (i % C != C - 1 && i != g1 - 1) continue;
+    for (int nb = 0; nb < NB; ++nb) { xa[nb][0] = xb[nb][0]; xa[nb][1] = xb[nb][1]; }
+    const bool seg_end = kc == C - 1 || i == g1 - 1;
+    const int seg_tile = tile;
+    kc = kcn;
+    if (kc == 0) ++tile;
+    kcn = kc + 1 == C ? 0 : kc + 1;
+    if (!seg_end) continue;
 
     // ---- end of a tile segment: k-group 1 hands its sums to k-group 0
-    const int tile = i / C;
 #pragma unroll
     for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
@@ -226,13 +239,13 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
           for (int e = 0; e < 4; ++e) red[(wi * PER + (mt * NB + nb) * 4 + e) * 32 + lane] = big[mt][nb][e];
     }
     consumers_sync();
-    const int t0 = tile * C;
+    const int t0 = seg_tile * C;
     const int cf = owner(t0, T, G), cl = owner(t0 + C - 1, T, G);
     const bool whole = cf == cl;
     const size_t seg_elems = (size_t)M * kTileN;
-    const float inv_scale = __ldg(P + (size_t)T * kBlockFloats + tile);
+    const float inv_scale = __ldg(P + (size_t)T * kBlockFloats + seg_tile);
     // my workspace slot: 0 if this tile holds my first chunk, else 1
-    float* part = ws + ((size_t)c * 2 + (g0 / C == tile ? 0 : 1)) * seg_elems;
+    float* part = ws + ((size_t)c * 2 + (g0 / C == seg_tile ? 0 : 1)) * seg_elems;
     if (kg == 0) {
 #pragma unroll
       for (int mt = 0; mt < MTW; ++mt)
@@ -246,7 +259,7 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
             const int m = 8 * nb + 2 * t + (e & 1);
             if (m < M) {
               if (whole) {
-                const int n = tile * kTileN + col;
+                const int n = seg_tile * kTileN + col;
                 if (n < N) {
                   if (epilogue == 1) v = fmaxf(v, 0.f);
                   else if (epilogue == 2) v = __fadd_rn(R[(size_t)m * ldr + n], v);
@@ -271,7 +284,7 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
     }
     __threadfence();
     consumers_sync();
-    if (tid == 0) last = atomicAdd(tickets + tile, 1) == cl - cf;
+    if (tid == 0) last = atomicAdd(tickets + seg_tile, 1) == cl - cf;
     consumers_sync();
     if (!last) continue;
     __threadfence();
@@ -295,7 +308,7 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
             acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
           }
       }
-      const int m = (4 * e4) / kTileN, n0 = tile * kTileN + (4 * e4) % kTileN;
+      const int m = (4 * e4) / kTileN, n0 = seg_tile * kTileN + (4 * e4) % kTileN;
       const float a4[4] = {acc.x, acc.y, acc.z, acc.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -307,7 +320,7 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
         Y[(size_t)m * ldy + n] = v;
       }
     }
-    if (tid == 0) tickets[tile] = 0;
+    if (tid == 0) tickets[seg_tile] = 0;
     consumers_sync();
   }
 }
@@ -347,8 +360,8 @@ __global__ void pack_kernel(const float* __restrict__ W, int ldw, int N, int K, 
   for (size_t u = blockIdx.x * (size_t)blockDim.x + threadIdx.x; u < units;
        u += (size_t)gridDim.x * blockDim.x) {
     const int lane = (int)(u & 31), part = (int)((u >> 5) & 1), mt = (int)((u >> 6) & 1);
-    const int wi = (int)((u >> 7) & 3), k16 = (int)((u >> 9) & 1);
-    const size_t blk = u >> 10;
+    const int wi = (int)((u >> 7) & 3), k16 = (int)((u >> 9) & 3);
+    const size_t blk = u >> 11;
     const int kc = (int)(blk % C), tile = (int)(blk / C);
     const int g = lane >> 2, t = lane & 3;
     const float sc = scale[tile];
@@ -389,13 +402,7 @@ inline int grid_for(int N, int K, int cps) {
   return (int)G;
 }
 
-inline int ctas_per_sm(int M) {
-  static const int v = [] {
-    const char* e = getenv("IG_PACKED_CPS");     // tuning sweeps only: 2 (default) or 3
-    return e && atoi(e) == 3 ? 3 : 2;
-  }();
-  return M <= 16 ? v : 1;
-}
+inline int ctas_per_sm(int M) { return M <= 16 ? 2 : 1; }
 
 template <int NB, int CPS, int STAGES>
 int launch(const float* X, int ldx, const float* P, float* Y, int ldy, const float* R, int ldr,
@@ -454,11 +461,7 @@ extern "C" int ig_sgemm_packed(const float* X, int ldx, const float* P, int N, i
   ig_sgemm_packed_sizes(M, N, K, nullptr, &ws_need, &tk_need);
   if (ws_need > workspace_floats || tk_need > ntickets) return IG_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
-  if (M > 16) return launch<4, 1, 12>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
-  if (ctas_per_sm(M) == 3) {
-    if (M <= 8) return launch<1, 3, 4>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
-    return launch<2, 3, 4>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
-  }
-  if (M <= 8) return launch<1, 2, 6>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
-  return launch<2, 2, 6>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
+  if (M > 16) return launch<4, 1, 6>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
+  if (M <= 8) return launch<1, 2, 3>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
+  return launch<2, 2, 3>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
 }

@@ -182,7 +182,7 @@ class DecodeEngine:
     def __init__(self, model, config: RunConfig, *, max_steps: int | None = None,
                  pool_dtype: str = "f16", device=None, group=None, fetch_ctas: int = 32,
                  fetch_threads: int = 32, fetch_priority: int = 0, hbm_layers: int = 0,
-                 fetch_impl: str = "tma", fetch_rows: int = 16, dense: str = "tc",
+                 fetch_impl: str = "tma", fetch_rows: int = 16, dense: str = "packed",
                  cuda_graph: bool = False, resident: bool | None = None, spec_stream: bool = True,
                  append_stream: bool = False):
         config.validate()
@@ -230,8 +230,8 @@ class DecodeEngine:
             raise ValueError("fetch_impl must be 'ldg' or 'tma'")
         self.fetch_impl = fetch_impl
         self.fetch_rows = fetch_rows
-        if dense not in ("ig", "tc", "cublas"):
-            raise ValueError("dense must be 'ig', 'tc' or 'cublas'")
+        if dense not in ("ig", "tc", "cublas", "packed"):
+            raise ValueError("dense must be 'ig', 'tc', 'cublas' or 'packed'")
         self.dense = dense
         self.cuda_graph = cuda_graph
         if cuda_graph and (config.record_selection or config.record_scores):
@@ -342,6 +342,14 @@ class DecodeEngine:
             ksp = self._ksplit(B, N_, K_)
             self.gemm_ksplit[(N_, K_)] = ksp
             ws = max(ws, ((N_ + 127) // 128) * ksp * B * 128)
+        self._packed = {}
+        if self.dense == "packed":
+            ws = 0
+            for N_, K_ in shapes:
+                wf = ctypes.c_size_t()
+                _lib.call("ig_sgemm_packed_sizes", B, N_, K_, None, ctypes.byref(wf), None, kernels=0)
+                ws = max(ws, wf.value)
+            self._pack_weights()
         self.gemm_ws = torch.empty(ws, dtype=f32, device=dev)
         self.gemm_tickets = torch.zeros(max((N_ + 127) // 128 for N_, _ in shapes), dtype=i32, device=dev)
         pf, tk = ctypes.c_size_t(), ctypes.c_size_t()
@@ -744,10 +752,48 @@ class DecodeEngine:
         lib = _lib.load()
         return lib.ig_sgemm_tc_ksplit(M, N, K) if self.dense == "tc" else lib.ig_sgemm_rows_ksplit(M, N, K)
 
+    def _pack_weights(self) -> None:
+        """dense="packed": re-lay every decode-step weight once into the
+        ig_sgemm_packed block format (same bytes as f32).  The row-major copies
+        stay for the prefill."""
+        spec_ = self.scheme == "speculative"
+        mats = []
+        for li in range(self.L):
+            fused = spec_ and li + 1 < self.L and self.wfused[li] is not None
+            mats += [self.wfused[li] if fused else self.wqkv[li], self.wo[li], self.ffn_in[li],
+                     self.ffn_out[li]]
+        for W in mats:
+            self._packed_weight(W)
+        torch.cuda.synchronize(self.device)
+
+    def _packed_weight(self, W):
+        key = (W.data_ptr(), W.shape[0], W.shape[1], W.stride(0))
+        P = self._packed.get(key)
+        if P is None:
+            K, N = W.shape
+            pf = ctypes.c_size_t()
+            _lib.call("ig_sgemm_packed_sizes", 1, N, K, ctypes.byref(pf), None, None, kernels=0)
+            P = torch.empty(pf.value, dtype=torch.float32, device=self.device)
+            _lib.call("ig_sgemm_pack", W.data_ptr(), W.stride(0), N, K, P.data_ptr(),
+                      torch.cuda.current_stream(self.device).cuda_stream, kernels=2)
+            self._packed[key] = P
+        return P
+
     def _gemm(self, X, W, Y, cs, epilogue: int = 0, R=None) -> None:
         """Y = X @ W (+ ReLU / + R) on the compute stream."""
         M, K = X.shape
         N = W.shape[1]
+        if self.dense == "packed":
+            P = self._packed_weight(W)
+            if self._inst is not None:
+                self._mark("dense", -1, self.compute, True, 4 * (K * N + M * K + M * N))
+            _lib.call("ig_sgemm_packed", X.data_ptr(), X.stride(0), P.data_ptr(), N, K, Y.data_ptr(),
+                      Y.stride(0), _lib.ptr(R), R.stride(0) if R is not None else 0, M, epilogue,
+                      self.gemm_ws.data_ptr(), self.gemm_ws.numel(), self.gemm_tickets.data_ptr(),
+                      self.gemm_tickets.numel(), cs)
+            if self._inst is not None:
+                self._mark("dense", -1, self.compute, False)
+            return
         if self.dense == "cublas":
             res = torch.addmm(R, X, W) if epilogue == 2 else torch.matmul(X, W)
             if epilogue == 1:

@@ -146,7 +146,7 @@ SPEC_RUNS = sorted(r for r in RUNS if RUNS[r]["scheme"] == "speculative")
 
 @pytest.mark.parametrize("rname", SPEC_RUNS)
 @pytest.mark.parametrize("mname", ["m64", "m256"])
-@pytest.mark.parametrize("dense", ["ig", "tc"])
+@pytest.mark.parametrize("dense", ["ig", "tc", "packed"])
 def test_resident_engine_matches_oracle(mname, rname, dense):
     """dense="tc": the projections on 3xTF32 tensor cores -- still every
     selection identical to the oracle's (f32-level x_a)."""
