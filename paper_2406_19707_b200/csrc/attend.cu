@@ -670,6 +670,7 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
   extern __shared__ __align__(128) uint8_t att_ring[];       // [warps][RING][16 rows][512 B]
   __shared__ float wm[kMmaWarps], wl[kMmaWarps];
   __shared__ float wacc[kMmaWarps][d];
+  pdl_trigger();
   __shared__ int last;
   const int b = blockIdx.z, h = blockIdx.y, c = blockIdx.x;
   const size_t bh = (size_t)b * Hg + h;
@@ -921,6 +922,7 @@ attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restric
                     float* __restrict__ out, int ldo) {
   constexpr int d = 128, NS = MmaT<T>::NS;
   extern __shared__ __align__(128) uint8_t wp_ring[];        // [warps][RING][slot]
+  pdl_trigger();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int maxseg = (cap + kWpSeg - 1) / kWpSeg;            // == max_chunks (scratch layout)

@@ -33,6 +33,14 @@ __device__ __forceinline__ float key_to_float(uint32_t k) {
   return __uint_as_float(u);
 }
 
+// Let a programmatic-dependent successor (the packed GEMM, launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization) start filling its weight
+// rings while this grid runs; the successor reads this grid's outputs only
+// after griddepcontrol.wait.  No effect on plainly launched successors.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -142,6 +142,13 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
   };
   if (tid == 0)
     for (int jj = 0; jj < kStages && g0 + jj < g1; ++jj) issue(jj, jj);
+  // Programmatic dependent launch: the weight stream above does not depend on
+  // the previous kernel, so this grid may start (and fill its rings) while
+  // that kernel drains; x, R, Y, the workspace and the tickets are touched
+  // only after the wait (full completion + visibility of the previous grid).
+  // The next GEMM may likewise launch as soon as SMs free up.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   // ---- kg = k-group (k16 steps 2 kg, 2 kg + 1 of a block), wi = 32-column
   // slab of the tile
@@ -402,6 +409,14 @@ inline int grid_for(int N, int K, int cps) {
   return (int)G;
 }
 
+inline bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("IG_PDL");             // A/B switch: IG_PDL=0 launches plainly
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
 inline int ctas_per_sm(int M) { return M <= 16 ? 2 : 1; }
 
 template <int NB, int CPS, int STAGES>
@@ -412,7 +427,18 @@ int launch(const float* X, int ldx, const float* P, float* Y, int ldy, const flo
   const size_t smem = (size_t)(STAGES * kBlockFloats + 4 * 2 * NB * 4 * 32) * sizeof(float);
   auto kern = sgemm_packed_kernel<NB, CPS, STAGES>;
   IG_CUDA_STATUS(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<G, kThreads, smem, s>>>(X, ldx, P, Y, ldy, R, ldr, M, N, K, C, epilogue, ws, tickets);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  IG_CUDA_STATUS(cudaLaunchKernelEx(&cfg, kern, X, ldx, P, Y, ldy, R, ldr, M, N, K, C, epilogue, ws,
+                                    tickets));
   IG_LAUNCH_STATUS();
   return IG_OK;
 }

@@ -17,6 +17,7 @@ __global__ void __launch_bounds__(kLnThreads)
 layernorm_kernel(const float* __restrict__ x, const float* __restrict__ g,
                  const float* __restrict__ bias, float eps, int D, float* __restrict__ out) {
   __shared__ double red[kLnThreads / kWarp];
+  pdl_trigger();
   const float* xr = x + (size_t)blockIdx.x * D;
   float* yr = out + (size_t)blockIdx.x * D;
   const bool cached = D <= kLnCache * kLnThreads;
