@@ -185,10 +185,14 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
   float4 xa[NB][2], xb[NB][2];
   int kc = g0 % C, tile = g0 / C;          // chunk g0 + j = (tile, kc)
   int kcn = kc + 1 == C ? 0 : kc + 1;      // row block of the next chunk
-  load_x(kc, true, xa);
+  load_x(kc, true, xb);
   int st = 0, ph = 0;                      // ring stage and its phase parity
 
   for (int j = 0, i = g0; i < g1; ++i, ++j) {
+    // xb (loaded one iteration ago) becomes current before the next block's
+    // load reuses it: the copy waits only if that load has not landed yet
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) { xa[nb][0] = xb[nb][0]; xa[nb][1] = xb[nb][1]; }
     load_x(kcn, i + 1 < g1, xb);
     if (tid == 0 && j >= 1 && i - 1 + kStages < g1) {
       const int sp = st == 0 ? kStages - 1 : st - 1;        // stage of iteration j - 1
@@ -221,8 +225,6 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
     __syncwarp();
     if (lane == 0) bar_arrive(empty_s + 8 * st);
     if (++st == kStages) { st = 0; ph ^= 1; }
-#pragma unroll
-    for (int nb = 0; nb < NB; ++nb) { xa[nb][0] = xb[nb][0]; xa[nb][1] = xb[nb][1]; }
     const bool seg_end = kc == C - 1 || i == g1 - 1;
     const int seg_tile = tile;
     kc = kcn;
