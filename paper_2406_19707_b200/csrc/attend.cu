@@ -912,7 +912,7 @@ constexpr int kWpWarps = 4;
 constexpr int kWpSlotBytes = kMmaTileBytes + 64 + 512;       // rows + ids + query row
 
 template <typename T, int RING>
-__global__ void __launch_bounds__(kWpWarps * 32, 3)
+__global__ void __launch_bounds__(kWpWarps * 32, RING <= 2 ? 3 : 2)
 attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_cur,
                     const float* __restrict__ v_cur, int ldkv, const T* __restrict__ stage,
                     const int32_t* __restrict__ idx, const int32_t* __restrict__ n_in,
@@ -990,13 +990,23 @@ attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restric
     if (it_lo < it_hi && geom(it_lo, bh, seg, r0, r1, ntl)) cur = it_lo;
     else if (it_lo < it_hi) cur = next_item(it_lo);
   }
+  // Issue cursor: runs up to RING - 1 tiles ahead of the compute cursor,
+  // across item boundaries (an empty item still takes its q-carrying slot).
+  long long icur = cur;
+  int itl = 0, ibh = 0, iseg = 0, ir0 = 0, ir1 = 0, intl = 0;
+  if (icur >= 0) geom(icur, ibh, iseg, ir0, ir1, intl);
   int slot_ctr = 0;                     // ring slot of the next tile to issue
-  if (cur >= 0) {
-    int bh, seg, r0, r1, ntl;
-    geom(cur, bh, seg, r0, r1, ntl);
-    issue(bh, r0, r1, 0, 0);            // tile 0 (maybe empty: still carries q)
-    slot_ctr = 1;
-  }
+  int pending = 0;                      // tiles issued and not yet consumed
+  auto issue_next = [&]() {
+    issue(ibh, ir0, ir1, itl, slot_ctr % RING);
+    ++slot_ctr;
+    ++pending;
+    if (++itl >= max(1, intl)) {
+      icur = next_item(icur);
+      itl = 0;
+      if (icur >= 0) geom(icur, ibh, iseg, ir0, ir1, intl);
+    }
+  };
   int cslot = 0;                        // ring slot of the tile being computed
   while (cur >= 0) {
     int bh, seg, r0, r1, ntl;
@@ -1011,23 +1021,13 @@ attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restric
     uint32_t bq[8][2];
     const int ntiles = max(1, ntl);     // an empty item still consumes its q-carrying slot
     for (int tl = 0; tl < ntiles; ++tl) {
-      // look ahead one tile: this item's next tile or the next item's first
-      bool issued = false;
-      if (tl + 1 < ntl) {
-        issue(bh, r0, r1, tl + 1, slot_ctr % RING);
-        issued = true;
-      } else if (nxt >= 0) {
-        int nbh, nseg, nr0, nr1, nntl;
-        geom(nxt, nbh, nseg, nr0, nr1, nntl);
-        issue(nbh, nr0, nr1, 0, slot_ctr % RING);
-        issued = true;
-      }
-      if (issued) {
-        ++slot_ctr;
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-      } else {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-      }
+      // keep RING tiles in the ring (this one included), then wait for this one
+      while (pending < RING && icur >= 0) issue_next();
+      if (pending >= 4) asm volatile("cp.async.wait_group 3;" ::: "memory");
+      else if (pending == 3) asm volatile("cp.async.wait_group 2;" ::: "memory");
+      else if (pending == 2) asm volatile("cp.async.wait_group 1;" ::: "memory");
+      else asm volatile("cp.async.wait_group 0;" ::: "memory");
+      --pending;
       __syncwarp();
       const uint32_t slot = sring + cslot * kWpSlotBytes;
       const uint8_t* gslot = wbase + (size_t)cslot * kWpSlotBytes;
@@ -1238,13 +1238,30 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
         }
         const int maxseg = (cap + kWpSeg - 1) / kWpSeg;
         const long long items = (long long)grid.z * grid.y * maxseg;
-        const int ctas = (int)min((long long)sms * 3, (items + kWpWarps - 1) / kWpWarps);
-        const size_t smem = (size_t)kWpWarps * 2 * kWpSlotBytes;
-        IG_CUDA_STATUS(cudaFuncSetAttribute(attend512_wp_kernel<T, 2>,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attend512_wp_kernel<T, 2><<<ctas, kWpWarps * 32, smem, s>>>(
-            q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, (int)grid.z,
-            (int)grid.y, cap, sqrt_d, max_chunks, partial, tickets, out, ldo);
+        // ring depth: 2 tiles per warp at 3 CTAs/SM (default) or 3 at 2 CTAs/SM
+        // (IG_WP_RING=3: more bytes in flight per SM, fewer warps -- measured
+        // 3.48 vs 3.76 TB/s at 819 rows, so per-warp latency, not bytes in
+        // flight, bounds this kernel)
+        static const int ring = [] {
+          const char* e = getenv("IG_WP_RING");
+          return e && atoi(e) == 3 ? 3 : 2;
+        }();
+        const int per_sm = ring == 2 ? 3 : 2;
+        const int ctas = (int)min((long long)sms * per_sm, (items + kWpWarps - 1) / kWpWarps);
+        const size_t smem = (size_t)kWpWarps * ring * kWpSlotBytes;
+        if (ring == 2) {
+          IG_CUDA_STATUS(cudaFuncSetAttribute(attend512_wp_kernel<T, 2>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          attend512_wp_kernel<T, 2><<<ctas, kWpWarps * 32, smem, s>>>(
+              q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, (int)grid.z,
+              (int)grid.y, cap, sqrt_d, max_chunks, partial, tickets, out, ldo);
+        } else {
+          IG_CUDA_STATUS(cudaFuncSetAttribute(attend512_wp_kernel<T, 3>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+          attend512_wp_kernel<T, 3><<<ctas, kWpWarps * 32, smem, s>>>(
+              q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, (int)grid.z,
+              (int)grid.y, cap, sqrt_d, max_chunks, partial, tickets, out, ldo);
+        }
         IG_LAUNCH_STATUS();
         return IG_OK;
       }
