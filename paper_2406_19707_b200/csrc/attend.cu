@@ -907,11 +907,11 @@ attend512_mma_kernel(const float* __restrict__ q, int ldq, const float* __restri
 // CTA-per-chunk kernel spent most of its time filling and draining its
 // pipeline once per 400-row chunk.
 // ---------------------------------------------------------------------------
-constexpr int kWpSeg = 128;                                  // rows per work item
+constexpr int kWpSegDefault = 128;                           // rows per work item
 constexpr int kWpWarps = 4;
 constexpr int kWpSlotBytes = kMmaTileBytes + 64 + 512;       // rows + ids + query row
 
-template <typename T, int RING>
+template <typename T, int RING, int kWpSeg>
 __global__ void __launch_bounds__(kWpWarps * 32, RING <= 2 ? 3 : 2)
 attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_cur,
                     const float* __restrict__ v_cur, int ldkv, const T* __restrict__ stage,
@@ -926,17 +926,20 @@ attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restric
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int maxseg = (cap + kWpSeg - 1) / kWpSeg;            // == max_chunks (scratch layout)
-  const long long items = (long long)B * Hg * maxseg;
-  const long long tw = (long long)gridDim.x * kWpWarps, gw = (long long)blockIdx.x * kWpWarps + w;
-  const long long per = (items + tw - 1) / tw;
-  const long long it_lo = gw * per, it_hi = min(items, it_lo + per);
+  // 32-bit item arithmetic (64-bit division is a subroutine call per item)
+  const int items = B * Hg * maxseg;
+  const int tw = gridDim.x * kWpWarps, gw = blockIdx.x * kWpWarps + w;
+  // ceil(items / tw) items per warp (the balanced floor/ceil split and 256-row
+  // items both measured slower at 819 rows: 74-77 vs 70 us)
+  const int per = (items + tw - 1) / tw;
+  const int it_lo = gw * per, it_hi = min(items, it_lo + per);
   uint8_t* wbase = wp_ring + (size_t)w * RING * kWpSlotBytes;
   const uint32_t sring = (uint32_t)__cvta_generic_to_shared(wbase);
 
   // item geometry; an item exists if seg < nseg(bh) (segment 0 always: the current row)
-  auto geom = [&](long long it, int& bh, int& seg, int& r0, int& r1, int& ntl) -> bool {
-    bh = (int)(it / maxseg);
-    seg = (int)(it - (long long)bh * maxseg);
+  auto geom = [&](int it, int& bh, int& seg, int& r0, int& r1, int& ntl) -> bool {
+    bh = it / maxseg;
+    seg = it - bh * maxseg;
     const int b = bh / Hg;
     const int rows = att_rows(rows_bh, n_in, st, b, (size_t)bh);
     const int nseg = max(1, (rows + kWpSeg - 1) / kWpSeg);
@@ -946,8 +949,8 @@ attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restric
     ntl = max(0, (r1 - r0 + 15) / 16);
     return true;
   };
-  auto next_item = [&](long long it) -> long long {        // first existing item > it
-    for (long long j = it + 1; j < it_hi; ++j) {
+  auto next_item = [&](int it) -> int {                    // first existing item > it
+    for (int j = it + 1; j < it_hi; ++j) {
       int bh, seg, r0, r1, ntl;
       if (geom(j, bh, seg, r0, r1, ntl)) return j;
     }
@@ -984,7 +987,7 @@ attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restric
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
-  long long cur = -1;
+  int cur = -1;
   {
     int bh, seg, r0, r1, ntl;
     if (it_lo < it_hi && geom(it_lo, bh, seg, r0, r1, ntl)) cur = it_lo;
@@ -992,7 +995,7 @@ attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restric
   }
   // Issue cursor: runs up to RING - 1 tiles ahead of the compute cursor,
   // across item boundaries (an empty item still takes its q-carrying slot).
-  long long icur = cur;
+  int icur = cur;
   int itl = 0, ibh = 0, iseg = 0, ir0 = 0, ir1 = 0, intl = 0;
   if (icur >= 0) geom(icur, ibh, iseg, ir0, ir1, intl);
   int slot_ctr = 0;                     // ring slot of the next tile to issue
@@ -1013,7 +1016,7 @@ attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restric
     geom(cur, bh, seg, r0, r1, ntl);
     const int b = bh / Hg, h = bh - b * Hg;
     const int pos = att_pos(pos_in, st, bh);
-    const long long nxt = next_item(cur);
+    const int nxt = next_item(cur);
     float m = -INFINITY, l = 0.f;
     float acc[8][4];
 #pragma unroll
@@ -1155,15 +1158,39 @@ attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restric
     if (lastw) {                        // merge every segment of (b, h) in order
       __threadfence();
       const float* pb = partial + (size_t)bh * max_chunks * (d + 2);
+      // lane i holds segment i's (m, l) (segments 32.. folded in order), so the
+      // max and the scales take one L2 round trip, not one per segment
       float MM = -INFINITY;
-      for (int i = 0; i < nseg; ++i) MM = fmaxf(MM, __ldcg(pb + (size_t)i * (d + 2)));
+      for (int i = lane; i < nseg; i += 32) MM = fmaxf(MM, __ldcg(pb + (size_t)i * (d + 2)));
+      MM = warp_max(MM);
       float LL = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int i = 0; i < nseg; ++i) {
-        const float mi = __ldcg(pb + (size_t)i * (d + 2));
-        const float sc = mi == -INFINITY ? 0.f : expf(mi - MM);
-        LL += __ldcg(pb + (size_t)i * (d + 2) + 1) * sc;
+      for (int i0 = 0; i0 < nseg; i0 += 32) {
+        const int i = i0 + lane;
+        float sc = 0.f, li = 0.f;
+        if (i < nseg) {
+          const float mi = __ldcg(pb + (size_t)i * (d + 2));
+          li = __ldcg(pb + (size_t)i * (d + 2) + 1);
+          sc = mi == -INFINITY ? 0.f : expf(mi - MM);
+        }
+        const int cnt = min(32, nseg - i0);
+        for (int j0 = 0; j0 < cnt; j0 += 8) {   // accumulator rows 8 segments per batch
+          float2 v[8][2];                      // rows are 8-B aligned ((d + 2) floats)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) o[e] += __ldcg(pb + (size_t)i * (d + 2) + 2 + lane * 4 + e) * sc;
+          for (int u = 0; u < 8; ++u)
+            if (j0 + u < cnt) {
+              const float2* r = reinterpret_cast<const float2*>(pb + (size_t)(i0 + j0 + u) * (d + 2) + 2);
+              v[u][0] = __ldcg(r + 2 * lane);
+              v[u][1] = __ldcg(r + 2 * lane + 1);
+            }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (j0 + u >= cnt) break;
+            const float scu = __shfl_sync(0xffffffffu, sc, j0 + u);
+            const float lu = __shfl_sync(0xffffffffu, li, j0 + u);
+            LL += lu * scu;
+            o[0] += v[u][0].x * scu; o[1] += v[u][0].y * scu; o[2] += v[u][1].x * scu; o[3] += v[u][1].y * scu;
+          }
+        }
       }
 #pragma unroll
       for (int e = 0; e < 4; ++e) out[(size_t)b * ldo + (size_t)h * d + lane * 4 + e] = o[e] / LL;
@@ -1236,32 +1263,36 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
               cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
             sms = 148;
         }
-        const int maxseg = (cap + kWpSeg - 1) / kWpSeg;
-        const long long items = (long long)grid.z * grid.y * maxseg;
         // ring depth: 2 tiles per warp at 3 CTAs/SM (default) or 3 at 2 CTAs/SM
         // (IG_WP_RING=3: more bytes in flight per SM, fewer warps -- measured
         // 3.48 vs 3.76 TB/s at 819 rows, so per-warp latency, not bytes in
-        // flight, bounds this kernel)
+        // flight, bounds this kernel); IG_WP_SEG=256: 256-row work items
         static const int ring = [] {
           const char* e = getenv("IG_WP_RING");
           return e && atoi(e) == 3 ? 3 : 2;
         }();
+        static const int seg = [] {
+          const char* e = getenv("IG_WP_SEG");
+          return e && atoi(e) == 256 ? 256 : kWpSegDefault;
+        }();
         const int per_sm = ring == 2 ? 3 : 2;
+        const int maxseg = (cap + seg - 1) / seg;
+        const long long items = (long long)grid.z * grid.y * maxseg;
         const int ctas = (int)min((long long)sms * per_sm, (items + kWpWarps - 1) / kWpWarps);
         const size_t smem = (size_t)kWpWarps * ring * kWpSlotBytes;
-        if (ring == 2) {
-          IG_CUDA_STATUS(cudaFuncSetAttribute(attend512_wp_kernel<T, 2>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          attend512_wp_kernel<T, 2><<<ctas, kWpWarps * 32, smem, s>>>(
-              q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, (int)grid.z,
-              (int)grid.y, cap, sqrt_d, max_chunks, partial, tickets, out, ldo);
-        } else {
-          IG_CUDA_STATUS(cudaFuncSetAttribute(attend512_wp_kernel<T, 3>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-          attend512_wp_kernel<T, 3><<<ctas, kWpWarps * 32, smem, s>>>(
-              q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, (int)grid.z,
-              (int)grid.y, cap, sqrt_d, max_chunks, partial, tickets, out, ldo);
-        }
+#define IG_ATT_WP(RING, SEG)                                                                    \
+  do {                                                                                         \
+    IG_CUDA_STATUS(cudaFuncSetAttribute(attend512_wp_kernel<T, RING, SEG>,                     \
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    attend512_wp_kernel<T, RING, SEG><<<ctas, kWpWarps * 32, smem, s>>>(                        \
+        q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, (int)grid.z,     \
+        (int)grid.y, cap, sqrt_d, max_chunks, partial, tickets, out, ldo);                      \
+  } while (0)
+        if (ring == 2 && seg == 256) IG_ATT_WP(2, 256);
+        else if (ring == 3 && seg == 256) IG_ATT_WP(3, 256);
+        else if (ring == 3) IG_ATT_WP(3, kWpSegDefault);
+        else IG_ATT_WP(2, kWpSegDefault);
+#undef IG_ATT_WP
         IG_LAUNCH_STATUS();
         return IG_OK;
       }
