@@ -45,12 +45,15 @@ namespace packed {
 constexpr int kTileN = 128;            // output columns per tile
 constexpr int kChunkK = 64;            // weight rows per block
 constexpr int kBlockFloats = kTileN * kChunkK;   // 8192 floats = 32 KB
-constexpr int kConsumerWarps = 8;
-constexpr int kThreads = kConsumerWarps * 32;
+// A CTA = KG k-groups x 4 column slabs of 32 columns: KG = 2 (8 warps, 2 CTAs
+// per SM) or KG = 4 (16 warps, 1 CTA per SM with a deeper ring); each k-group
+// takes 4 / KG of a block's k16 steps.
 // (CTAs per SM, ring stages): M <= 16 runs 2 x 3 (96-KB rings); M <= 32 (64
 // accumulator registers per lane) 1 x 6.  Registers: an SM
 // sub-partition holds 16K, i.e. 2 CTAs x 8 warps -> 128 per thread, 3 -> 80.
-template <int CPS> struct RegCap { static constexpr int v = CPS == 1 ? 255 : (CPS == 2 ? 128 : 80); };
+template <int WARPS_PER_SM> struct RegCap {   // 64K registers per SM, 16K per sub-partition
+  static constexpr int v = WARPS_PER_SM <= 8 ? 255 : (WARPS_PER_SM <= 16 ? 128 : 80);
+};
 
 __device__ __forceinline__ void bar_init(uint32_t bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
@@ -72,8 +75,9 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
       ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
+template <int THREADS>
 __device__ __forceinline__ void consumers_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(THREADS) : "memory");
 }
 
 constexpr float kLoScale = 2048.f;           // lo parts carry the next 11 bits
@@ -100,8 +104,8 @@ __device__ __forceinline__ void mma_h(float* c, const uint4& a, uint32_t b0, uin
 __device__ __forceinline__ int owner(int x, int T, int G) { return (int)(((long)(x + 1) * G - 1) / T); }
 __device__ __forceinline__ int first_chunk(int c, int T, int G) { return (int)((long)c * T / G); }
 
-template <int NB, int CPS, int kStages>   // NB 8-sequence MMA n tiles: M <= 8 NB
-__global__ void __launch_bounds__(kThreads) __maxnreg__(RegCap<CPS>::v)
+template <int NB, int CPS, int kStages, int KG>   // NB 8-sequence MMA n tiles: M <= 8 NB
+__global__ void __launch_bounds__(KG * 4 * 32) __maxnreg__(RegCap<CPS * KG * 4>::v)
 sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ P,
                     float* __restrict__ Y, int ldy, const float* __restrict__ R, int ldr, int M,
                     int N, int K, int C, int epilogue, float* __restrict__ ws,
@@ -109,8 +113,9 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
   extern __shared__ __align__(128) float smem[];
   constexpr int MTW = 2;                        // m16 tiles per warp (32 columns)
   constexpr int PER = MTW * NB * 4;             // accumulator floats per lane
+  constexpr int kWarps = KG * 4, kSteps = 4 / KG;
   float* ring = smem;                                        // [kStages][4096]
-  float* red = smem + kStages * kBlockFloats;                // [4 warps][PER][32]
+  float* red = smem + kStages * kBlockFloats;                // [KG-1][4 warps][PER][32]
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   __shared__ int last;
 
@@ -126,7 +131,7 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       bar_init(full_s + 8 * s, 1);
-      bar_init(empty_s + 8 * s, kConsumerWarps);
+      bar_init(empty_s + 8 * s, kWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -169,20 +174,20 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
 #pragma unroll
   for (int nb = 0; nb < NB; ++nb) {
     mok[nb] = 8 * nb + g < M;
-    xrow[nb] = X + (size_t)(mok[nb] ? 8 * nb + g : 0) * ldx + 32 * kg + 4 * t;
+    xrow[nb] = X + (size_t)(mok[nb] ? 8 * nb + g : 0) * ldx + kSteps * 16 * kg + 4 * t;
   }
-  auto load_x = [&](int kc, bool ok, float4 (&xv)[NB][2]) {
+  auto load_x = [&](int kc, bool ok, float4 (&xv)[NB][kSteps]) {
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-      for (int s2 = 0; s2 < 2; ++s2) {
-        const int k = kc * kChunkK + 32 * kg + 16 * s2 + 4 * t;
+      for (int s2 = 0; s2 < kSteps; ++s2) {
+        const int k = kc * kChunkK + kSteps * 16 * kg + 16 * s2 + 4 * t;
         xv[nb][s2] = (ok && mok[nb] && k < K)
                          ? __ldg(reinterpret_cast<const float4*>(xrow[nb] + kc * kChunkK + 16 * s2))
                          : make_float4(0.f, 0.f, 0.f, 0.f);
       }
   };
-  float4 xa[NB][2], xb[NB][2];
+  float4 xa[NB][kSteps], xb[NB][kSteps];
   int kc = g0 % C, tile = g0 / C;          // chunk g0 + j = (tile, kc)
   int kcn = kc + 1 == C ? 0 : kc + 1;      // row block of the next chunk
   load_x(kc, true, xb);
@@ -202,8 +207,8 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
     bar_wait(full_s + 8 * st, ph);
     const uint4* blk = reinterpret_cast<const uint4*>(ring + st * kBlockFloats);
 #pragma unroll
-    for (int s2 = 0; s2 < 2; ++s2) {
-      const int k16 = 2 * kg + s2;
+    for (int s2 = 0; s2 < kSteps; ++s2) {
+      const int k16 = kSteps * kg + s2;
       uint4 a[MTW][2];
 #pragma unroll
       for (int mt = 0; mt < MTW; ++mt)
@@ -239,15 +244,16 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
       for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
         for (int e = 0; e < 4; ++e) big[mt][nb][e] = fmaf(small[mt][nb][e], kLoScaleInv, big[mt][nb][e]);
-    if (kg == 1) {
+    if (kg > 0) {
 #pragma unroll
       for (int mt = 0; mt < MTW; ++mt)
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) red[(wi * PER + (mt * NB + nb) * 4 + e) * 32 + lane] = big[mt][nb][e];
+          for (int e = 0; e < 4; ++e)
+            red[(((kg - 1) * 4 + wi) * PER + (mt * NB + nb) * 4 + e) * 32 + lane] = big[mt][nb][e];
     }
-    consumers_sync();
+    consumers_sync<kWarps * 32>();
     const int t0 = seg_tile * C;
     const int cf = owner(t0, T, G), cl = owner(t0 + C - 1, T, G);
     const bool whole = cf == cl;
@@ -262,7 +268,11 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
         for (int nb = 0; nb < NB; ++nb) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            float v = (big[mt][nb][e] + red[(wi * PER + (mt * NB + nb) * 4 + e) * 32 + lane]) * inv_scale;
+            float v = big[mt][nb][e];
+#pragma unroll
+            for (int gg = 1; gg < KG; ++gg)             // k-groups in fixed order
+              v += red[(((gg - 1) * 4 + wi) * PER + (mt * NB + nb) * 4 + e) * 32 + lane];
+            v *= inv_scale;
             // C fragment: e = 0/1 -> (column g, seq 2t / 2t+1), e = 2/3 -> (column g + 8, ...)
             const int col = 32 * wi + 16 * mt + g + 8 * (e >> 1);
             const int m = 8 * nb + 2 * t + (e & 1);
@@ -288,13 +298,13 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
 #pragma unroll
         for (int e = 0; e < 4; ++e) big[mt][nb][e] = small[mt][nb][e] = 0.f;
     if (whole) {
-      consumers_sync();          // red is rewritten at the next segment end
+      consumers_sync<kWarps * 32>();          // red is rewritten at the next segment end
       continue;
     }
     __threadfence();
-    consumers_sync();
+    consumers_sync<kWarps * 32>();
     if (tid == 0) last = atomicAdd(tickets + seg_tile, 1) == cl - cf;
-    consumers_sync();
+    consumers_sync<kWarps * 32>();
     if (!last) continue;
     __threadfence();
     // segment s of the tile = CTA cf + s; only CTA cf can have started in an
@@ -303,7 +313,7 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
     // segments, not one per segment), in segment order.
     const int nseg = cl - cf + 1;
     const float* seg0 = ws + ((size_t)cf * 2 + (first_chunk(cf, T, G) < t0 ? 1 : 0)) * seg_elems;
-    for (int e4 = tid; e4 < M * (kTileN / 4); e4 += kConsumerWarps * 32) {
+    for (int e4 = tid; e4 < M * (kTileN / 4); e4 += kWarps * 32) {
       float4 acc = __ldcg(reinterpret_cast<const float4*>(seg0) + e4);
       for (int sg = 1; sg < nseg; sg += 8) {
         float4 v[8];
@@ -330,7 +340,7 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
       }
     }
     if (tid == 0) tickets[seg_tile] = 0;
-    consumers_sync();
+    consumers_sync<kWarps * 32>();
   }
 }
 
@@ -419,19 +429,28 @@ inline bool pdl_enabled() {
   return v;
 }
 
-inline int ctas_per_sm(int M) { return M <= 16 ? 2 : 1; }
+inline int ctas_per_sm(int M) {
+  // IG_PACKED_CTA=16: one 16-warp CTA per SM with a 6-deep ring (more bytes in
+  // flight, fewer CTA fix-ups) -- measured equal or slower (ffn_out 4.7 vs 5.6
+  // TB/s), so 2 x 8-warp CTAs stay the default
+  static const int wide = [] {
+    const char* e = getenv("IG_PACKED_CTA");
+    return e && atoi(e) == 16 ? 1 : 0;
+  }();
+  return M <= 16 && !wide ? 2 : 1;
+}
 
-template <int NB, int CPS, int STAGES>
+template <int NB, int CPS, int STAGES, int KG>
 int launch(const float* X, int ldx, const float* P, float* Y, int ldy, const float* R, int ldr,
            int M, int N, int K, int epilogue, float* ws, int32_t* tickets, cudaStream_t s) {
   const int C = (K + kChunkK - 1) / kChunkK;
   const int G = grid_for(N, K, CPS);
-  const size_t smem = (size_t)(STAGES * kBlockFloats + 4 * 2 * NB * 4 * 32) * sizeof(float);
-  auto kern = sgemm_packed_kernel<NB, CPS, STAGES>;
+  const size_t smem = (size_t)(STAGES * kBlockFloats + (KG - 1) * 4 * 2 * NB * 4 * 32) * sizeof(float);
+  auto kern = sgemm_packed_kernel<NB, CPS, STAGES, KG>;
   IG_CUDA_STATUS(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(KG * 4 * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -489,7 +508,11 @@ extern "C" int ig_sgemm_packed(const float* X, int ldx, const float* P, int N, i
   ig_sgemm_packed_sizes(M, N, K, nullptr, &ws_need, &tk_need);
   if (ws_need > workspace_floats || tk_need > ntickets) return IG_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
-  if (M > 16) return launch<4, 1, 6>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
-  if (M <= 8) return launch<1, 2, 3>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
-  return launch<2, 2, 3>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
+  if (M > 16) return launch<4, 1, 6, 2>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
+  if (ctas_per_sm(M) == 1) {      // 16 warps, 6-deep ring
+    if (M <= 8) return launch<1, 1, 6, 4>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
+    return launch<2, 1, 6, 4>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
+  }
+  if (M <= 8) return launch<1, 2, 3, 2>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
+  return launch<2, 2, 3, 2>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
 }
