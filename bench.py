@@ -201,7 +201,10 @@ def run_reference_arm(a) -> None:
 def _config(a) -> dict:
     from paper_2406_19707_b200.model import SHAPES
     sh = SHAPES[a.shape]
-    return {"workload": WORKLOAD["name"], "model": a.shape, "layers": a.layers or sh["layers"],
+    default = (a.shape, a.batch, a.prompt) == (WORKLOAD["shape"], WORKLOAD["batch"], WORKLOAD["prompt"])
+    name = WORKLOAD["name"] if default else (f"{a.shape.upper()}-shaped decode, batch {a.batch}, "
+                                             f"{a.prompt}-token context (non-default config)")
+    return {"workload": name, "model": a.shape, "layers": a.layers or sh["layers"],
             "model_dim": sh["model_dim"], "heads": sh["heads"], "ffn_dim": sh["ffn_dim"],
             "global_batch": a.batch, "context": a.prompt, "partial_ratio": WORKLOAD["ratio"],
             "alpha": WORKLOAD["alpha"], "cap_ratio": WORKLOAD["cap"],

@@ -431,3 +431,99 @@ def test_select_all_rows_and_single_row():
         np.testing.assert_array_equal(picks[h], O.topk_indices(sc[h], 37))
     picks, n = G.select_tokens([np.array([2.5], np.float32)], G.SpeculationConfig())
     assert n == 1 and list(picks[0]) == [0]
+
+
+@pytest.mark.parametrize("env", [{"IG_PDL": "0"}, {"IG_PACKED_CTA": "16"}])
+def test_sgemm_packed_launch_variants(env):
+    """A chained pair of packed GEMMs (FFN-in with ReLU -> FFN-out with residual,
+    the decode step's pattern) in a subprocess per launch variant: with PDL off
+    the bits equal the default (PDL on) run -- the programmatic overlap never
+    lets a GEMM read its input early; the one-CTA-per-SM grid (other stream-K
+    segmentation) agrees within f32 summation-order noise."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    code = (
+        "import numpy as np, torch, ctypes, sys\n"
+        "from paper_2406_19707_b200 import _lib\n"
+        "g = torch.Generator(device='cuda'); g.manual_seed(11)\n"
+        "M, D, F = 16, 1024, 4096\n"
+        "x = torch.randn(M, D, device='cuda', generator=g)\n"
+        "w1 = torch.randn(D, F, device='cuda', generator=g) * 0.03\n"
+        "w2 = torch.randn(F, D, device='cuda', generator=g) * 0.03\n"
+        "def pack(W):\n"
+        "    K, N = W.shape\n"
+        "    pf, wf, tf = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()\n"
+        "    _lib.call('ig_sgemm_packed_sizes', M, N, K, ctypes.byref(pf), ctypes.byref(wf), ctypes.byref(tf), kernels=0)\n"
+        "    P = torch.empty(pf.value, device='cuda')\n"
+        "    _lib.call('ig_sgemm_pack', W.data_ptr(), N, N, K, P.data_ptr(), _lib.stream_handle())\n"
+        "    return P, wf.value, tf.value\n"
+        "(p1, w1f, t1), (p2, w2f, t2) = pack(w1), pack(w2)\n"
+        "ws = torch.empty(max(w1f, w2f), device='cuda'); tk = torch.zeros(max(t1, t2), dtype=torch.int32, device='cuda')\n"
+        "h = torch.empty(M, F, device='cuda'); y = torch.empty(M, D, device='cuda')\n"
+        "outs = []\n"
+        "for _ in range(3):\n"
+        "    _lib.call('ig_sgemm_packed', x.data_ptr(), D, p1.data_ptr(), F, D, h.data_ptr(), F, None, 0, M, 1, ws.data_ptr(), ws.numel(), tk.data_ptr(), tk.numel(), _lib.stream_handle())\n"
+        "    _lib.call('ig_sgemm_packed', h.data_ptr(), F, p2.data_ptr(), D, F, y.data_ptr(), D, x.data_ptr(), D, M, 2, ws.data_ptr(), ws.numel(), tk.data_ptr(), tk.numel(), _lib.stream_handle())\n"
+        "    outs.append(y.cpu().numpy().copy())\n"
+        "assert all((o == outs[0]).all() for o in outs)\n"
+        "ref = (torch.relu(x.double() @ w1.double()) @ w2.double() + x.double()).cpu().numpy()\n"
+        "np.save(sys.argv[1], outs[0]); np.save(sys.argv[1] + '.ref.npy', ref)\n")
+    res = {}
+    with tempfile.TemporaryDirectory() as td:
+        for name, e in (("default", {}), ("variant", env)):
+            f = os.path.join(td, name + ".npy")
+            r = subprocess.run([sys.executable, "-c", code, f], env=dict(os.environ, **e),
+                               capture_output=True, text=True, timeout=300)
+            assert r.returncode == 0, r.stderr[-2000:]
+            res[name] = np.load(f)
+        ref = np.load(os.path.join(td, "default.npy") + ".ref.npy")
+    np.testing.assert_allclose(res["default"], ref, rtol=1e-5, atol=1e-4)
+    if "IG_PDL" in env:
+        np.testing.assert_array_equal(res["variant"], res["default"])
+    else:
+        np.testing.assert_allclose(res["variant"], res["default"], rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("env", [{"IG_WP_RING": "3"}, {"IG_WP_SEG": "256"}])
+def test_attend_wp_variants_match_default(env):
+    """The warp-persistent attention's opt-in ring depth / item size (per-process
+    switches, so each in a subprocess) produce the default kernel's outputs over
+    ragged slot tables (fixed-order merges: bit-identical per item size; the
+    256-row items merge fewer segments, so f32 rounding may differ)."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    code = (
+        "import numpy as np, torch, ctypes, sys\n"
+        "from paper_2406_19707_b200 import _lib\n"
+        "g = torch.Generator(device='cuda'); g.manual_seed(5)\n"
+        "B, Hg, d, cap = 4, 5, 128, 900\n"
+        "q = torch.randn(B, 3 * Hg * d, device='cuda', generator=g)\n"
+        "stage = torch.randn(B, Hg, cap, 2 * d, device='cuda', generator=g).half()\n"
+        "slot = torch.arange(cap, device='cuda', dtype=torch.int32).repeat(B, Hg, 1).contiguous()\n"
+        "slot[:, :, 7] = -1\n"
+        "used = torch.tensor([[cap, 819, 300, 1, 640]] * B, dtype=torch.int32, device='cuda')\n"
+        "pos = torch.full((B, Hg), 5, dtype=torch.int32, device='cuda')\n"
+        "st = torch.zeros(8, dtype=torch.int32, device='cuda')\n"
+        "pf, tk = ctypes.c_size_t(), ctypes.c_size_t()\n"
+        "_lib.call('ig_attend_scratch', B, Hg, d, cap, ctypes.byref(pf), ctypes.byref(tk), kernels=0)\n"
+        "part = torch.empty(pf.value, device='cuda'); tick = torch.zeros(tk.value, dtype=torch.int32, device='cuda')\n"
+        "out = torch.empty(B, Hg * d, device='cuda')\n"
+        "ld = q.stride(0); Hgd = Hg * d\n"
+        "_lib.call('ig_attend_slots', q.data_ptr(), ld, q.data_ptr() + 4 * Hgd, q.data_ptr() + 8 * Hgd, ld, stage.data_ptr(), 1, slot.data_ptr(), used.data_ptr(), pos.data_ptr(), st.data_ptr(), B, Hg, d, cap, part.data_ptr(), tick.data_ptr(), out.data_ptr(), Hgd, _lib.stream_handle())\n"
+        "np.save(sys.argv[1], out.cpu().numpy())\n")
+    res = {}
+    with tempfile.TemporaryDirectory() as td:
+        for name, e in (("default", {}), ("variant", env)):
+            f = os.path.join(td, name + ".npy")
+            r = subprocess.run([sys.executable, "-c", code, f], env=dict(os.environ, **e),
+                               capture_output=True, text=True, timeout=300)
+            assert r.returncode == 0, r.stderr[-2000:]
+            res[name] = np.load(f)
+    if "IG_WP_RING" in env:
+        np.testing.assert_array_equal(res["variant"], res["default"])
+    else:
+        np.testing.assert_allclose(res["variant"], res["default"], rtol=1e-5, atol=1e-6)
