@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -356,9 +357,11 @@ class DecodeEngine:
         _lib.call("ig_attend_scratch", B, Hg, d, S, ctypes.byref(pf), ctypes.byref(tk), kernels=0)
         self.att_partial = torch.empty(pf.value, dtype=f32, device=dev)
         self.att_tickets = torch.zeros(tk.value, dtype=i32, device=dev)
-        self.compute = torch.cuda.Stream(device=dev)
+        # stream priorities (IG_STREAM_PRIO = "compute,spec"; tuning A/B only)
+        cprio, sprio = (int(v) for v in os.environ.get("IG_STREAM_PRIO", "0,-1").split(","))
+        self.compute = torch.cuda.Stream(device=dev, priority=cprio)
         self.fetch_stream = torch.cuda.Stream(device=dev, priority=self.fetch_priority)
-        self.spec_stream = torch.cuda.Stream(device=dev, priority=-1)
+        self.spec_stream = torch.cuda.Stream(device=dev, priority=sprio)
         self.append_stream = torch.cuda.Stream(device=dev)
         self.ev_q = [torch.cuda.Event() for _ in range(L)]
         self.ev_qkv = [torch.cuda.Event() for _ in range(L)]
