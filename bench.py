@@ -410,7 +410,7 @@ def run_b200(a) -> None:
                 hbm[k] = {"achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
                           "frac": gbs / hbm_peak, "bytes_per_launch": iso[k]["bytes"],
                           "ms_per_launch": iso[k]["ms"],
-                          "how": f"alone on the GPU (fetch stream idle), layer {eng.L // 2}, best of 5"}
+                          "how": f"alone on the GPU (fetch stream idle), layer {eng.L // 2}, 10 launches back to back per event pair, best of 5"}
                 if k == "rehearse_count" and tr and "rehearse_count" in tr:
                     hbm[k]["traffic"] = iso[k]["bytes"] * tr["rehearse_count"]["dram_per_algorithmic"]
         for k in ("rehearse", "attend", "select"):          # in situ, sharing the GPU with the gather

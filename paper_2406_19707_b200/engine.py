@@ -701,15 +701,19 @@ class DecodeEngine:
         Hgd = Hg * d
         n_tot = int(self.n[li].sum().item())
 
-        def best(fn):
+        def best(fn, chain=10):
+            # `chain` launches between one event pair: a lone launch's time would
+            # include the host's launch latency (~10-20 us at these sizes)
+            fn()
             t = []
             for _ in range(reps):
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(cs)
-                fn()
+                for _ in range(chain):
+                    fn()
                 e1.record(cs)
                 e1.synchronize()
-                t.append(e0.elapsed_time(e1))
+                t.append(e0.elapsed_time(e1) / chain)
             return min(t)
 
         def rehearse():
