@@ -71,3 +71,58 @@ def test_two_rank_head_parallel_matches_oracle():
         assert hg == 2
         assert err < 1e-4, (rank, rname, err)
         assert mism == 0, (rank, rname, mism)
+
+
+def _nccl_graph_worker(port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from tests.golden_cfg import models, run_config
+        from tests.test_engine_gpu import engine_cfg, oracle_sessions
+        from paper_2406_19707_b200 import DecodeEngine
+        _, sk = models("m64")
+        ocfg = run_config("spec_counter", gen_len=6)
+        sessions = oracle_sessions(sk, ocfg)
+        outs = {}
+        for name, kw in (("eager", dict(group=dist.group.WORLD)),
+                         ("graph", dict(group=dist.group.WORLD, cuda_graph=True)),
+                         ("plain", {})):
+            eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg, record_selection=False),
+                                             copy.deepcopy(sessions), pool_dtype="f32", **kw)
+            outs[name] = np.stack([eng.decode_step().cpu().numpy().copy()
+                                   for _ in range(ocfg.gen_len)])
+            eng.close()
+        q.put(("ok", outs))
+    except Exception as e:  # surface the failure to the parent
+        q.put(("error", repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_group_graph_capture_matches_eager():
+    """The N > 1 code path (NCCL all-reduces of the head-count sums on the
+    speculation stream and of the W_O / FFN-out partials on the compute stream)
+    captured into a CUDA graph and replayed: on a one-rank NCCL group (the only
+    NCCL group one GPU can host) the replayed steps equal the eager steps of the
+    same group and of the group-less engine bit for bit."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_graph_worker, args=(port, q))
+    p.start()
+    status, res = q.get(timeout=600)
+    p.join(timeout=120)
+    assert status == "ok", res
+    np.testing.assert_array_equal(res["graph"], res["eager"])
+    np.testing.assert_array_equal(res["eager"], res["plain"])
