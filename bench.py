@@ -242,7 +242,8 @@ def run_b200(a) -> None:
         else:
             dist.init_process_group("gloo")
         group = dist.group.WORLD
-    if world > 1 and a.cuda_graph and a.dist_backend != "nccl":
+    if (world > 1 and a.cuda_graph and a.dist_backend != "nccl"
+            and os.environ.get("IG_PEER_AR", "1") == "0"):
         a.cuda_graph = False            # gloo collectives cannot be captured
     sh = dict(SHAPES[a.shape])
     if a.layers:

@@ -251,6 +251,31 @@ int ig_sgemm_packed(const float* X, int ldx, const float* packed, int N, int K, 
                     const float* R, int ldr, int M, int epilogue, float* workspace,
                     size_t workspace_floats, int32_t* tickets, size_t ntickets, void* stream);
 
+/* ---- head-parallel output all-reduce over peer memory (N > 1) ----------
+ * Replaces the NCCL all-reduce of the row-parallel W_O / FFN-out partials
+ * (engine.py:360-364 sums over all heads).  Each rank allocates a receive
+ * buffer (2 x world x n 4-B elements) and flags (2 x world u32 + a 16-B ticket) with
+ * ig_peer_alloc, shares them by CUDA IPC (ig_ipc_get_handle / _open_handle;
+ * 64-B handles), and passes device arrays of the world's receive / flag base
+ * pointers.  ig_allreduce_peer pushes `src` (n floats) into every rank's slot,
+ * raises its flag, waits for all ranks and writes out = sum over ranks (rank
+ * order, identical bits on every rank) + residual (may be NULL).  `call` in
+ * [0, calls_per_step) numbers the all-reduces of one step (epoch from
+ * st->step: graph-replayable); ticket = flags + 2 * world (u32).          */
+int ig_peer_alloc(int n, int world, void** recv, void** flags);
+int ig_peer_free(void* recv, void* flags);
+int ig_ipc_get_handle(void* dev_ptr, void* handle64);
+int ig_ipc_open_handle(const void* handle64, void** dev_ptr);
+int ig_ipc_close(void* dev_ptr);
+int ig_allreduce_peer(const float* src, int n, const uint64_t* peer_recv, const uint64_t* peer_flags,
+                      int rank, int world, const ig_step_state* st, int call, int calls_per_step,
+                      const float* residual, float* out, uint32_t* ticket, void* stream);
+/* The same for the per-sequence int32 head-count sums (speculation.py:154-158:
+ * n averages over ALL heads); no residual. */
+int ig_allreduce_peer_i32(const int32_t* src, int n, const uint64_t* peer_recv,
+                          const uint64_t* peer_flags, int rank, int world, const ig_step_state* st,
+                          int call, int calls_per_step, int32_t* out, uint32_t* ticket, void* stream);
+
 /* ---- step bookkeeping -------------------------------------------------- */
 /* s_len = min(s_len + 1, limit), seq += 2, step += 1 (engine.py:377-378). */
 int ig_step_advance(ig_step_state* st, void* stream);

@@ -60,6 +60,13 @@ _SIGS = {
     "ig_sgemm_packed_sizes": [_I, _I, _I, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ),
                               ctypes.POINTER(_SZ)],
     "ig_sgemm_pack": [_P, _I, _I, _I, _P, _P],
+    "ig_peer_alloc": [_I, _I, ctypes.POINTER(_P), ctypes.POINTER(_P)],
+    "ig_peer_free": [_P, _P],
+    "ig_ipc_get_handle": [_P, _P],
+    "ig_ipc_open_handle": [_P, ctypes.POINTER(_P)],
+    "ig_ipc_close": [_P],
+    "ig_allreduce_peer": [_P, _I, _P, _P, _I, _I, _P, _I, _I, _P, _P, _P, _P],
+    "ig_allreduce_peer_i32": [_P, _I, _P, _P, _I, _I, _P, _I, _I, _P, _P, _P],
     "ig_sgemm_packed": [_P, _I, _P, _I, _I, _P, _I, _P, _I, _I, _I, _P, _SZ, _P, _SZ, _P],
     "ig_step_advance": [_P, _P],
     "ig_layernorm": [_P, _P, _P, _F, _I, _I, _P, _P],

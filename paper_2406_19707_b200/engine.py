@@ -112,6 +112,66 @@ class HostPool:
             pass
 
 
+class PeerAllReduce:
+    """The head-parallel output all-reduce over peer memory (csrc/collective.cu):
+    every rank's receive buffer and flags are mapped into every other rank by
+    CUDA IPC (handles exchanged once through the process group); one kernel per
+    call pushes this rank's partial into every rank, waits for all of them and
+    sums in rank order (+ residual).  Replaces the NCCL all-reduce of the W_O /
+    FFN-out partials (engine.py:360-364)."""
+
+    def __init__(self, n: int, group, device, dtype=torch.float32):
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        self.n = n
+        self.fn = {torch.float32: "ig_allreduce_peer", torch.int32: "ig_allreduce_peer_i32"}[dtype]
+        recv, flags = ctypes.c_void_p(), ctypes.c_void_p()
+        _lib.call("ig_peer_alloc", n, self.world, ctypes.byref(recv), ctypes.byref(flags), kernels=0)
+        self.recv, self.flags = recv.value, flags.value
+        self._opened = []
+        try:
+            hr, hf = (ctypes.c_char * 64)(), (ctypes.c_char * 64)()
+            _lib.call("ig_ipc_get_handle", self.recv, hr, kernels=0)
+            _lib.call("ig_ipc_get_handle", self.flags, hf, kernels=0)
+            objs = [None] * self.world
+            dist.all_gather_object(objs, (bytes(hr), bytes(hf)), group=group)
+            pr, pf = [], []
+            for r, (h_r, h_f) in enumerate(objs):
+                if r == self.rank:
+                    pr.append(self.recv)
+                    pf.append(self.flags)
+                    continue
+                for h, lst in ((h_r, pr), (h_f, pf)):
+                    ptr = ctypes.c_void_p()
+                    buf = (ctypes.c_char * 64).from_buffer_copy(h)
+                    _lib.call("ig_ipc_open_handle", buf, ctypes.byref(ptr), kernels=0)
+                    self._opened.append(ptr.value)
+                    lst.append(ptr.value)
+            self.peer_recv = torch.tensor(pr, dtype=torch.int64, device=device)
+            self.peer_flags = torch.tensor(pf, dtype=torch.int64, device=device)
+            self.ticket = self.flags + 4 * 2 * self.world
+        except Exception:
+            self.close()
+            raise
+
+    def __call__(self, src, out, residual, st, call: int, calls: int, stream: int) -> None:
+        if self.fn == "ig_allreduce_peer_i32":
+            _lib.call(self.fn, src.data_ptr(), self.n, self.peer_recv.data_ptr(),
+                      self.peer_flags.data_ptr(), self.rank, self.world, st.data_ptr(), call, calls,
+                      out.data_ptr(), self.ticket, stream)
+            return
+        _lib.call(self.fn, src.data_ptr(), self.n, self.peer_recv.data_ptr(),
+                  self.peer_flags.data_ptr(), self.rank, self.world, st.data_ptr(), call, calls,
+                  _lib.ptr(residual), out.data_ptr(), self.ticket, stream)
+
+    def close(self) -> None:
+        for p in self._opened:
+            _lib.call("ig_ipc_close", p, kernels=0)
+        self._opened = []
+        if self.recv:
+            _lib.call("ig_peer_free", self.recv, self.flags, kernels=0)
+            self.recv = self.flags = None
+
+
 def _simulate_prefill_rows(n: int, limit: int | None, policy: EvictionPolicy):
     """Row of each prompt token and the resulting metadata when N prompt rows
     are appended to an empty pool (engine.py:265-266 -> pool.py:53-81).  All
@@ -237,7 +297,11 @@ class DecodeEngine:
         self.cuda_graph = cuda_graph
         if cuda_graph and (config.record_selection or config.record_scores):
             raise ValueError("cuda_graph cannot record traces (host reads every layer)")
-        if cuda_graph and group is not None and dist.get_backend(group) != "nccl":
+        # N > 1: the step's collectives over peer memory (IG_PEER_AR=0: the process group)
+        self.use_peer = (group is not None and dist.get_world_size(group) > 1
+                         and os.environ.get("IG_PEER_AR", "1") != "0")
+        if (cuda_graph and group is not None and not self.use_peer
+                and dist.get_backend(group) != "nccl"):
             raise ValueError("cuda_graph needs NCCL for the collectives")
         self._graph = None
         self._graph_mode = False
@@ -256,6 +320,11 @@ class DecodeEngine:
         self.scale = float(np.float32(1.0 / np.sqrt(d)))   # speculation.py:127
         self._load_weights(model)
         self._alloc()
+        # N > 1: the W_O / FFN-out all-reduces over peer memory (IG_PEER_AR=0: NCCL)
+        self.peer_ar = self.peer_cnt = None
+        if self.use_peer:
+            self.peer_ar = PeerAllReduce(self.B * self.D, group, self.device)
+            self.peer_cnt = PeerAllReduce(self.B, group, self.device, torch.int32)
         self.s_host = 0
         self._inst = None
         self.iteration = 0
@@ -969,7 +1038,10 @@ class DecodeEngine:
                                   self.counts.data_ptr(), self.count_sum[nxt].data_ptr(), sps)
                         self._mark("rehearse", nxt, SP, False)
                         self._mark("select", nxt, SP, True)
-                        if self.world > 1:
+                        if self.peer_cnt is not None:
+                            self.peer_cnt(self.count_sum[nxt], self.count_sum[nxt], None, self.st,
+                                          nxt, L, sps)
+                        elif self.world > 1:
                             with torch.cuda.stream(SP):
                                 dist.all_reduce(self.count_sum[nxt], group=self.group)
                         _lib.call("ig_select", self.scores.data_ptr(),
@@ -1061,8 +1133,11 @@ class DecodeEngine:
                 self.ev_att[li].record(C)
                 if self.world > 1:
                     self._gemm(self.attn, self.wo[li], self.o, cs)
-                    dist.all_reduce(self.o, group=self.group)
-                    self.o.add_(x)                              # x_mid = x + attn_out
+                    if self.peer_ar is not None:                # x_mid = x + sum of partials
+                        self.peer_ar(self.o, self.o, x, self.st, 2 * li, 2 * L, cs)
+                    else:
+                        dist.all_reduce(self.o, group=self.group)
+                        self.o.add_(x)                          # x_mid = x + attn_out
                 else:
                     self._gemm(self.attn, self.wo[li], self.o, cs, epilogue=2, R=x)
                 _lib.call("ig_layernorm", self.o.data_ptr(), g2.data_ptr(), b2.data_ptr(),
@@ -1071,8 +1146,11 @@ class DecodeEngine:
                 x_new = self.xbuf[1] if x is self.xbuf[0] else self.xbuf[0]
                 if self.Fg != self.F:               # row-parallel FFN-out: sum the ranks
                     self._gemm(self.hidden, self.ffn_out[li], x_new, cs)
-                    dist.all_reduce(x_new, group=self.group)
-                    x_new.add_(self.o)
+                    if self.peer_ar is not None:
+                        self.peer_ar(x_new, x_new, self.o, self.st, 2 * li + 1, 2 * L, cs)
+                    else:
+                        dist.all_reduce(x_new, group=self.group)
+                        x_new.add_(self.o)
                 else:
                     self._gemm(self.hidden, self.ffn_out[li], x_new, cs, epilogue=2, R=self.o)
                 if recording:
@@ -1180,6 +1258,10 @@ class DecodeEngine:
 
     def close(self) -> None:
         self.pool.close()
+        for name in ("peer_ar", "peer_cnt"):
+            if getattr(self, name, None) is not None:
+                getattr(self, name).close()
+                setattr(self, name, None)
 
 
 def run(model, config: RunConfig, *, prompts=None, **kw):

@@ -44,15 +44,21 @@ def _worker(rank, world, port, q):
                         mism += r["n_selected"] != rr["n_selected"]
                         for hl, sel in enumerate(r["selected"]):
                             mism += set(sel) != set(rr["selected"][eng.h0 + hl])
+            peer = eng.peer_ar is not None
             eng.close()
-            q.put((rank, rname, err, mism, eng.Hg))
+            q.put((rank, rname, err, mism, (eng.Hg, peer)))
     except Exception as e:  # surface the failure to the parent
         q.put((rank, "error", repr(e), -1, 0))
     finally:
         dist.destroy_process_group()
 
 
-def test_two_rank_head_parallel_matches_oracle():
+@pytest.mark.parametrize("peer", ["1", "0"])
+def test_two_rank_head_parallel_matches_oracle(peer, monkeypatch):
+    """peer = 1 (default): the W_O / FFN-out all-reduces run over peer memory
+    (ig_allreduce_peer, buffers mapped by CUDA IPC between the two processes);
+    peer = 0: through the process group (gloo here, NCCL on a multi-GPU box)."""
+    monkeypatch.setenv("IG_PEER_AR", peer)
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
@@ -66,9 +72,9 @@ def test_two_rank_head_parallel_matches_oracle():
     res = [q.get(timeout=600) for _ in range(4)]
     for p in procs:
         p.join(timeout=120)
-    for rank, rname, err, mism, hg in res:
+    for rank, rname, err, mism, info in res:
         assert rname != "error", err
-        assert hg == 2
+        assert info == (2, peer == "1")
         assert err < 1e-4, (rank, rname, err)
         assert mism == 0, (rank, rname, mism)
 
@@ -126,3 +132,126 @@ def test_nccl_group_graph_capture_matches_eager():
     assert status == "ok", res
     np.testing.assert_array_equal(res["graph"], res["eager"])
     np.testing.assert_array_equal(res["eager"], res["plain"])
+
+
+def _peer_ar_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2406_19707_b200.engine import PeerAllReduce
+        n = 4 * 1024 + 12
+        ar = PeerAllReduce(n, dist.group.WORLD, torch.device("cuda", 0))
+        st = torch.zeros(8, dtype=torch.int32, device="cuda")
+        outs = []
+        for step in range(3):                    # epochs from the device step counter
+            st[4] = step                         # ig_step_state.step (int32 at byte 16)
+            for call in range(4):
+                g = torch.Generator(device="cuda")
+                g.manual_seed(1000 * step + 10 * call + rank)
+                src = torch.randn(n, device="cuda", generator=g)
+                res = torch.full((n,), float(call), device="cuda")
+                out = torch.empty(n, device="cuda")
+                ar(src, out, res if call % 2 else None, st, call, 4, torch.cuda.current_stream().cuda_stream)
+                outs.append(out.cpu().numpy())
+        ar.close()
+        q.put((rank, outs))
+    except Exception as e:  # surface the failure to the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_allreduce_sums_in_rank_order():
+    """ig_allreduce_peer between two processes (IPC-mapped buffers on one GPU):
+    out = p0 + p1 (+ residual) bit-identical on both ranks, across calls whose
+    slots alternate by parity and epochs that come from the device step
+    counter; ragged n (not a multiple of the grid)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 33000 + int.from_bytes(os.urandom(2), "little") % 2000
+    procs = [ctx.Process(target=_peer_ar_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+    assert not isinstance(res[0], str), res[0]
+    assert not isinstance(res[1], str), res[1]
+    n = 4 * 1024 + 12
+    k = 0
+    for step in range(3):
+        for call in range(4):
+            parts = []
+            for r in range(2):
+                g = torch.Generator(device="cuda")
+                g.manual_seed(1000 * step + 10 * call + r)
+                parts.append(torch.randn(n, device="cuda", generator=g).cpu().numpy())
+            exp = parts[0] + parts[1]
+            if call % 2:
+                exp = exp + np.float32(call)
+            np.testing.assert_array_equal(res[0][k], exp)
+            np.testing.assert_array_equal(res[1][k], res[0][k])
+            k += 1
+
+
+def _graph_peer_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from tests.golden_cfg import models, run_config
+        from tests.test_engine_gpu import engine_cfg, oracle_sessions, oracle_decode
+        from paper_2406_19707_b200 import DecodeEngine
+        _, sk = models("m64")
+        ocfg = run_config("spec_counter", gen_len=6)
+        sessions = oracle_sessions(sk, ocfg)
+        ref_out, _ = oracle_decode(copy.deepcopy(sessions), ocfg.gen_len)
+        outs = {}
+        for graph in (False, True):
+            eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg, record_selection=False),
+                                             copy.deepcopy(sessions), pool_dtype="f32",
+                                             group=dist.group.WORLD, cuda_graph=graph)
+            assert eng.peer_ar is not None and eng.peer_cnt is not None
+            outs[graph] = np.stack([eng.decode_step().cpu().numpy().copy()
+                                    for _ in range(ocfg.gen_len)], axis=1)
+            eng.close()
+        err = float(np.abs(outs[True] - ref_out[:, 1:]).max() / max(1.0, np.abs(ref_out).max()))
+        q.put((rank, bool((outs[True] == outs[False]).all()), err))
+    except Exception as e:  # surface the failure to the parent
+        q.put((rank, repr(e), -1.0))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_graph_replay_over_peer_memory():
+    """With every collective of the step on peer memory (head-count sums and
+    W_O / FFN-out partials), the two-rank head-parallel step is captured into a
+    CUDA graph even over gloo: replayed steps equal eager steps bit for bit and
+    stay within 1e-4 of the unsharded oracle."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 35000 + int.from_bytes(os.urandom(2), "little") % 2000
+    procs = [ctx.Process(target=_graph_peer_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+    for rank, same, err in res:
+        assert same is True, (rank, same)
+        assert err < 1e-4, (rank, err)
