@@ -70,9 +70,13 @@ allreduce_peer_kernel(const T* __restrict__ src, int n, const uint64_t* __restri
   }
   // 3. wait for every rank's slot, sum in rank order, add the residual
   const uint32_t* my_flags = reinterpret_cast<const uint32_t*>(peer_flags[rank]) + par * G;
-  if (tid < G)
-    while (ld_acquire_sys(my_flags + tid) != epoch) {
-    }
+  if (tid < G) {
+    // a peer that never arrives (broken mapping, a rank that died) must fail
+    // the context loudly, not hang the GPU: trap after ~10 s of spinning
+    const long long t0 = clock64();
+    while (ld_acquire_sys(my_flags + tid) != epoch)
+      if (clock64() - t0 > 20000000000LL) __trap();
+  }
   __syncthreads();
   const T* base = reinterpret_cast<const T*>(peer_recv[rank]) + (size_t)par * G * n;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + tid; i < (size_t)nv; i += stride) {
