@@ -925,7 +925,16 @@ attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restric
   pdl_trigger();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int maxseg = (cap + kWpSeg - 1) / kWpSeg;            // == max_chunks (scratch layout)
+  // Items are laid out over the segments the LARGEST row set of this launch
+  // needs (read from the device-side counts: every warp computes the same
+  // value), not over cap: layers whose selections are well below cap would
+  // otherwise leave empty item slots in some warps' ranges and a tail of
+  // warps with full ranges.
+  int maxrows = 0;
+  for (int i = lane; i < B * Hg; i += 32) maxrows = max(maxrows, att_rows(rows_bh, n_in, st, i / Hg, (size_t)i));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) maxrows = max(maxrows, __shfl_xor_sync(0xffffffffu, maxrows, o));
+  const int maxseg = max(1, min((cap + kWpSeg - 1) / kWpSeg, (maxrows + kWpSeg - 1) / kWpSeg));
   // 32-bit item arithmetic (64-bit division is a subroutine call per item)
   const int items = B * Hg * maxseg;
   const int tw = gridDim.x * kWpWarps, gw = blockIdx.x * kWpWarps + w;
