@@ -323,8 +323,29 @@ class DecodeEngine:
         # N > 1: the W_O / FFN-out all-reduces over peer memory (IG_PEER_AR=0: NCCL)
         self.peer_ar = self.peer_cnt = None
         if self.use_peer:
-            self.peer_ar = PeerAllReduce(self.B * self.D, group, self.device)
-            self.peer_cnt = PeerAllReduce(self.B, group, self.device, torch.int32)
+            try:
+                self.peer_ar = PeerAllReduce(self.B * self.D, group, self.device)
+                self.peer_cnt = PeerAllReduce(self.B, group, self.device, torch.int32)
+            except Exception as e:  # noqa: BLE001 -- no IPC / peer access on this box
+                # every rank must take the same path: agree on it through the group
+                import sys
+                sys.stderr.write(f"DecodeEngine: peer-memory all-reduce unavailable ({e!r}); "
+                                 "using the process group\n")
+                for name in ("peer_ar", "peer_cnt"):
+                    if getattr(self, name) is not None:
+                        getattr(self, name).close()
+                        setattr(self, name, None)
+            ok = torch.tensor([1 if self.peer_cnt is not None else 0], dtype=torch.int32,
+                              device=self.device if dist.get_backend(group) == "nccl" else "cpu")
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+            if int(ok.item()) == 0:
+                for name in ("peer_ar", "peer_cnt"):
+                    if getattr(self, name) is not None:
+                        getattr(self, name).close()
+                        setattr(self, name, None)
+                self.use_peer = False
+                if cuda_graph and dist.get_backend(group) != "nccl":
+                    raise ValueError("cuda_graph needs NCCL or the peer-memory all-reduce")
         self.s_host = 0
         self._inst = None
         self.iteration = 0
