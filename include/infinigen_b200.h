@@ -270,6 +270,20 @@ int ig_ipc_close(void* dev_ptr);
 int ig_allreduce_peer(const float* src, int n, const uint64_t* peer_recv, const uint64_t* peer_flags,
                       int rank, int world, const ig_step_state* st, int call, int calls_per_step,
                       const float* residual, float* out, uint32_t* ticket, void* stream);
+/* The collective's push folded into the producer: ig_sgemm_packed_peer runs the
+ * packed GEMM (epilogue 0) and writes its final values into slot
+ * [parity][rank] of every rank's receive buffer (n = M * N, row-major) and
+ * raises this rank's flags when the whole grid is done (`done`: a u32 counter,
+ * zeroed once, left zeroed -- flags + 2 * world + 1); ig_allreduce_peer_sum
+ * then waits and sums (+ residual) without a push phase. */
+int ig_sgemm_packed_peer(const float* X, int ldx, const float* packed, int N, int K, int M,
+                         const uint64_t* peer_recv, const uint64_t* peer_flags, int rank, int world,
+                         const ig_step_state* st, int call, int calls_per_step, uint32_t* done,
+                         float* workspace, size_t workspace_floats, int32_t* tickets,
+                         size_t ntickets, void* stream);
+int ig_allreduce_peer_sum(int n, const uint64_t* peer_recv, const uint64_t* peer_flags, int rank,
+                          int world, const ig_step_state* st, int call, int calls_per_step,
+                          const float* residual, float* out, void* stream);
 /* The same for the per-sequence int32 head-count sums (speculation.py:154-158:
  * n averages over ALL heads); no residual. */
 int ig_allreduce_peer_i32(const int32_t* src, int n, const uint64_t* peer_recv,

@@ -67,6 +67,9 @@ _SIGS = {
     "ig_ipc_close": [_P],
     "ig_allreduce_peer": [_P, _I, _P, _P, _I, _I, _P, _I, _I, _P, _P, _P, _P],
     "ig_allreduce_peer_i32": [_P, _I, _P, _P, _I, _I, _P, _I, _I, _P, _P, _P],
+    "ig_sgemm_packed_peer": [_P, _I, _P, _I, _I, _I, _P, _P, _I, _I, _P, _I, _I, _P, _P, _SZ, _P, _SZ,
+                             _P],
+    "ig_allreduce_peer_sum": [_I, _P, _P, _I, _I, _P, _I, _I, _P, _P, _P],
     "ig_sgemm_packed": [_P, _I, _P, _I, _I, _P, _I, _P, _I, _I, _I, _P, _SZ, _P, _SZ, _P],
     "ig_step_advance": [_P, _P],
     "ig_layernorm": [_P, _P, _P, _F, _I, _I, _P, _P],

@@ -37,7 +37,7 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 
 // V = 4: float4 slices (n % 4 == 0, 16-B aligned); V = 1: scalar (any n, and
 // the int32 head-count sums)
-template <typename T, int V>
+template <typename T, int V, bool PUSH>
 __global__ void __launch_bounds__(kArThreads)
 allreduce_peer_kernel(const T* __restrict__ src, int n, const uint64_t* __restrict__ peer_recv,
                       const uint64_t* __restrict__ peer_flags, int rank, int G,
@@ -53,7 +53,9 @@ allreduce_peer_kernel(const T* __restrict__ src, int n, const uint64_t* __restri
   const int tid = threadIdx.x;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const VT* sv = reinterpret_cast<const VT*>(src);
-  // 1. push my partial into slot [par][rank] of every rank
+  // 1. push my partial into slot [par][rank] of every rank (PUSH = false: the
+  //    producer -- the packed GEMM's epilogue, ig_sgemm_packed_peer -- did it)
+  if constexpr (PUSH) {
   for (int r = 0; r < G; ++r) {
     VT* dv = reinterpret_cast<VT*>(reinterpret_cast<T*>(peer_recv[r]) + ((size_t)par * G + rank) * n);
     for (size_t i = blockIdx.x * (size_t)blockDim.x + tid; i < (size_t)nv; i += stride) dv[i] = sv[i];
@@ -67,6 +69,7 @@ allreduce_peer_kernel(const T* __restrict__ src, int n, const uint64_t* __restri
     if (tid == 0) *ticket = 0u;
     __threadfence_system();
     st_release_sys(reinterpret_cast<uint32_t*>(peer_flags[tid]) + par * G + rank, epoch);
+  }
   }
   // 3. wait for every rank's slot, sum in rank order, add the residual
   const uint32_t* my_flags = reinterpret_cast<const uint32_t*>(peer_flags[rank]) + par * G;
@@ -141,11 +144,11 @@ extern "C" int ig_ipc_close(void* dev_ptr) {
 }
 
 namespace ig {
-template <typename T>
+template <typename T, bool PUSH = true>
 static int allreduce_peer(const T* src, int n, const uint64_t* peer_recv, const uint64_t* peer_flags,
                           int rank, int world, const ig_step_state* st, int call, int calls_per_step,
                           const T* residual, T* out, uint32_t* ticket, void* stream) {
-  if (!src || !peer_recv || !peer_flags || !st || !out || !ticket || n < 1 || world < 1 ||
+  if ((PUSH && (!src || !ticket)) || !peer_recv || !peer_flags || !st || !out || n < 1 || world < 1 ||
       world > kArThreads || rank < 0 || rank >= world || call < 0 || call >= calls_per_step)
     return IG_EINVAL;
   const bool vec = std::is_same<T, float>::value && (n & 3) == 0 && !((uintptr_t)src & 15) &&
@@ -156,10 +159,10 @@ static int allreduce_peer(const T* src, int n, const uint64_t* peer_recv, const 
   if (blocks > 64) blocks = 64;
   cudaStream_t s = (cudaStream_t)stream;
   if (vec)
-    allreduce_peer_kernel<T, 4><<<blocks, kArThreads, 0, s>>>(
+    allreduce_peer_kernel<T, 4, PUSH><<<blocks, kArThreads, 0, s>>>(
         src, n, peer_recv, peer_flags, rank, world, st, call, calls_per_step, residual, out, ticket);
   else
-    allreduce_peer_kernel<T, 1><<<blocks, kArThreads, 0, s>>>(
+    allreduce_peer_kernel<T, 1, PUSH><<<blocks, kArThreads, 0, s>>>(
         src, n, peer_recv, peer_flags, rank, world, st, call, calls_per_step, residual, out, ticket);
   IG_LAUNCH_STATUS();
   return IG_OK;
@@ -180,4 +183,12 @@ extern "C" int ig_allreduce_peer_i32(const int32_t* src, int n, const uint64_t* 
                                      int32_t* out, uint32_t* ticket, void* stream) {
   return ig::allreduce_peer<int32_t>(src, n, peer_recv, peer_flags, rank, world, st, call,
                                      calls_per_step, nullptr, out, ticket, stream);
+}
+
+extern "C" int ig_allreduce_peer_sum(int n, const uint64_t* peer_recv, const uint64_t* peer_flags,
+                                     int rank, int world, const ig_step_state* st, int call,
+                                     int calls_per_step, const float* residual, float* out,
+                                     void* stream) {
+  return ig::allreduce_peer<float, false>(nullptr, n, peer_recv, peer_flags, rank, world, st, call,
+                                          calls_per_step, residual, out, nullptr, stream);
 }

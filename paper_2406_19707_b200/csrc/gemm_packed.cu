@@ -100,6 +100,18 @@ __device__ __forceinline__ void mma_h(float* c, const uint4& a, uint32_t b0, uin
       : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
 }
 
+// Optional all-reduce push (head-parallel W_O / FFN-out, csrc/collective.cu):
+// final values go to slot [parity][rank] of every rank's IPC-mapped receive
+// buffer instead of Y, and the grid's last CTA raises this rank's flag in
+// every rank -- the collective's push folded into the GEMM epilogue.
+struct PeerOut {
+  const uint64_t* recv = nullptr;    // [world] receive-buffer bases (u64)
+  const uint64_t* flags = nullptr;   // [world] flag-array bases
+  const ig_step_state* st = nullptr;
+  uint32_t* done = nullptr;          // grid-completion counter (local, left zeroed)
+  int rank = 0, world = 1, call = 0, calls = 1;
+};
+
 // chunk index -> CTA that owns it, for the split [c T / G, (c+1) T / G)
 __device__ __forceinline__ int owner(int x, int T, int G) { return (int)(((long)(x + 1) * G - 1) / T); }
 __device__ __forceinline__ int first_chunk(int c, int T, int G) { return (int)((long)c * T / G); }
@@ -109,7 +121,7 @@ __global__ void __launch_bounds__(KG * 4 * 32) __maxnreg__(RegCap<CPS * KG * 4>:
 sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restrict__ P,
                     float* __restrict__ Y, int ldy, const float* __restrict__ R, int ldr, int M,
                     int N, int K, int C, int epilogue, float* __restrict__ ws,
-                    int32_t* __restrict__ tickets) {
+                    int32_t* __restrict__ tickets, const PeerOut po) {
   extern __shared__ __align__(128) float smem[];
   constexpr int MTW = 2;                        // m16 tiles per warp (32 columns)
   constexpr int PER = MTW * NB * 4;             // accumulator floats per lane
@@ -154,6 +166,21 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
   // The next GEMM may likewise launch as soon as SMs free up.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  uint32_t po_epoch = 0;
+  size_t po_off = 0;                      // my slot within every rank's receive buffer
+  if (po.recv != nullptr) {
+    const uint32_t seqno = (uint32_t)po.st->step * (uint32_t)po.calls + (uint32_t)po.call;
+    po_epoch = seqno + 1u;
+    po_off = ((size_t)(seqno & 1u) * po.world + po.rank) * (size_t)M * N;
+  }
+  auto store = [&](int m, int n, float v) {
+    if (po.recv == nullptr) {
+      Y[(size_t)m * ldy + n] = v;
+    } else {
+      for (int r = 0; r < po.world; ++r)
+        reinterpret_cast<float*>(po.recv[r])[po_off + (size_t)m * N + n] = v;
+    }
+  };
 
   // ---- kg = k-group (k16 steps 2 kg, 2 kg + 1 of a block), wi = 32-column
   // slab of the tile
@@ -282,7 +309,7 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
                 if (n < N) {
                   if (epilogue == 1) v = fmaxf(v, 0.f);
                   else if (epilogue == 2) v = __fadd_rn(R[(size_t)m * ldr + n], v);
-                  Y[(size_t)m * ldy + n] = v;
+                  store(m, n, v);
                 }
               } else {
                 part[(size_t)m * kTileN + col] = v;
@@ -336,11 +363,26 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
         float v = a4[q];
         if (epilogue == 1) v = fmaxf(v, 0.f);
         else if (epilogue == 2) v = __fadd_rn(R[(size_t)m * ldr + n], v);
-        Y[(size_t)m * ldy + n] = v;
+        store(m, n, v);
       }
     }
     if (tid == 0) tickets[seg_tile] = 0;
     consumers_sync<kWarps * 32>();
+  }
+  if (po.recv != nullptr) {               // every final value of this grid is pushed
+    consumers_sync<kWarps * 32>();
+    if (tid == 0) {
+      __threadfence_system();
+      if (atomicAdd(po.done, 1u) == gridDim.x - 1) {
+        *po.done = 0u;
+        __threadfence_system();
+        const int par = (int)((po_epoch - 1u) & 1u);
+        for (int r = 0; r < po.world; ++r)
+          asm volatile("st.release.sys.global.u32 [%0], %1;"
+                       ::"l"(reinterpret_cast<uint32_t*>(po.flags[r]) + par * po.world + po.rank),
+                       "r"(po_epoch) : "memory");
+      }
+    }
   }
 }
 
@@ -442,7 +484,8 @@ inline int ctas_per_sm(int M) {
 
 template <int NB, int CPS, int STAGES, int KG>
 int launch(const float* X, int ldx, const float* P, float* Y, int ldy, const float* R, int ldr,
-           int M, int N, int K, int epilogue, float* ws, int32_t* tickets, cudaStream_t s) {
+           int M, int N, int K, int epilogue, float* ws, int32_t* tickets, cudaStream_t s,
+           const PeerOut& po) {
   const int C = (K + kChunkK - 1) / kChunkK;
   const int G = grid_for(N, K, CPS);
   const size_t smem = (size_t)(STAGES * kBlockFloats + (KG - 1) * 4 * 2 * NB * 4 * 32) * sizeof(float);
@@ -459,7 +502,7 @@ int launch(const float* X, int ldx, const float* P, float* Y, int ldy, const flo
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   IG_CUDA_STATUS(cudaLaunchKernelEx(&cfg, kern, X, ldx, P, Y, ldy, R, ldr, M, N, K, C, epilogue, ws,
-                                    tickets));
+                                    tickets, po));
   IG_LAUNCH_STATUS();
   return IG_OK;
 }
@@ -494,25 +537,58 @@ extern "C" int ig_sgemm_pack(const float* W, int ldw, int N, int K, float* P, vo
   return IG_OK;
 }
 
-extern "C" int ig_sgemm_packed(const float* X, int ldx, const float* P, int N, int K, float* Y,
-                               int ldy, const float* R, int ldr, int M, int epilogue,
-                               float* workspace, size_t workspace_floats, int32_t* tickets,
-                               size_t ntickets, void* stream) {
-  using namespace ig::packed;
-  if (!X || !P || !Y || !workspace || !tickets || M < 1 || M > 32 || N < 1 || K < 1 || ldx < K ||
-      ldy < N || epilogue < 0 || epilogue > 2 || (epilogue == 2 && (!R || ldr < N)))
+namespace ig {
+namespace packed {
+static int sgemm_packed_any(const float* X, int ldx, const float* P, int N, int K, float* Y, int ldy,
+                            const float* R, int ldr, int M, int epilogue, float* workspace,
+                            size_t workspace_floats, int32_t* tickets, size_t ntickets,
+                            cudaStream_t s, const PeerOut& po) {
+  if (!X || !P || (!Y && !po.recv) || !workspace || !tickets || M < 1 || M > 32 || N < 1 || K < 1 ||
+      ldx < K || (Y && ldy < N) || epilogue < 0 || epilogue > 2 || (epilogue == 2 && (!R || ldr < N)))
     return IG_EINVAL;
   if (((uintptr_t)P & 15) || ((uintptr_t)X & 15) || ((uintptr_t)workspace & 15) || (ldx & 3) || (K & 3))
     return IG_EINVAL;                                  // 16-B bulk copies and x vectors
   size_t ws_need = 0, tk_need = 0;
   ig_sgemm_packed_sizes(M, N, K, nullptr, &ws_need, &tk_need);
   if (ws_need > workspace_floats || tk_need > ntickets) return IG_EINVAL;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (M > 16) return launch<4, 1, 6, 2>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
+  if (M > 16) return launch<4, 1, 6, 2>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s, po);
   if (ctas_per_sm(M) == 1) {      // 16 warps, 6-deep ring
-    if (M <= 8) return launch<1, 1, 6, 4>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
-    return launch<2, 1, 6, 4>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
+    if (M <= 8) return launch<1, 1, 6, 4>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s, po);
+    return launch<2, 1, 6, 4>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s, po);
   }
-  if (M <= 8) return launch<1, 2, 3, 2>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
-  return launch<2, 2, 3, 2>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s);
+  if (M <= 8) return launch<1, 2, 3, 2>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s, po);
+  return launch<2, 2, 3, 2>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s, po);
+}
+}  // namespace packed
+}  // namespace ig
+
+extern "C" int ig_sgemm_packed(const float* X, int ldx, const float* P, int N, int K, float* Y,
+                               int ldy, const float* R, int ldr, int M, int epilogue,
+                               float* workspace, size_t workspace_floats, int32_t* tickets,
+                               size_t ntickets, void* stream) {
+  if (!Y) return IG_EINVAL;
+  return ig::packed::sgemm_packed_any(X, ldx, P, N, K, Y, ldy, R, ldr, M, epilogue, workspace,
+                                      workspace_floats, tickets, ntickets, (cudaStream_t)stream,
+                                      ig::packed::PeerOut{});
+}
+
+extern "C" int ig_sgemm_packed_peer(const float* X, int ldx, const float* P, int N, int K, int M,
+                                    const uint64_t* peer_recv, const uint64_t* peer_flags, int rank,
+                                    int world, const ig_step_state* st, int call, int calls_per_step,
+                                    uint32_t* done, float* workspace, size_t workspace_floats,
+                                    int32_t* tickets, size_t ntickets, void* stream) {
+  if (!peer_recv || !peer_flags || !st || !done || world < 1 || rank < 0 || rank >= world ||
+      call < 0 || call >= calls_per_step)
+    return IG_EINVAL;
+  ig::packed::PeerOut po;
+  po.recv = peer_recv;
+  po.flags = peer_flags;
+  po.st = st;
+  po.done = done;
+  po.rank = rank;
+  po.world = world;
+  po.call = call;
+  po.calls = calls_per_step;
+  return ig::packed::sgemm_packed_any(X, ldx, P, N, K, nullptr, N, nullptr, 0, M, 0, workspace,
+                                      workspace_floats, tickets, ntickets, (cudaStream_t)stream, po);
 }

@@ -163,6 +163,19 @@ class PeerAllReduce:
                   self.peer_flags.data_ptr(), self.rank, self.world, st.data_ptr(), call, calls,
                   _lib.ptr(residual), out.data_ptr(), self.ticket, stream)
 
+    def gemm_push(self, X, P, N: int, K: int, st, call: int, calls: int, ws, tickets, stream) -> None:
+        """The packed GEMM whose epilogue pushes X . W into every rank's slot."""
+        _lib.call("ig_sgemm_packed_peer", X.data_ptr(), X.stride(0), P.data_ptr(), N, K, X.shape[0],
+                  self.peer_recv.data_ptr(), self.peer_flags.data_ptr(), self.rank, self.world,
+                  st.data_ptr(), call, calls, self.ticket + 4, ws.data_ptr(), ws.numel(),
+                  tickets.data_ptr(), tickets.numel(), stream)
+
+    def sum(self, out, residual, st, call: int, calls: int, stream: int) -> None:
+        """Wait for every rank's push of `call`; out = sum over ranks + residual."""
+        _lib.call("ig_allreduce_peer_sum", self.n, self.peer_recv.data_ptr(),
+                  self.peer_flags.data_ptr(), self.rank, self.world, st.data_ptr(), call, calls,
+                  _lib.ptr(residual), out.data_ptr(), stream)
+
     def close(self) -> None:
         for p in self._opened:
             _lib.call("ig_ipc_close", p, kernels=0)
@@ -322,6 +335,9 @@ class DecodeEngine:
         self._alloc()
         # N > 1: the W_O / FFN-out all-reduces over peer memory (IG_PEER_AR=0: NCCL)
         self.peer_ar = self.peer_cnt = None
+        # the W_O / FFN-out push folded into the packed GEMM's epilogue (IG_PEER_FUSE=0: a
+        # separate push + sum kernel after a plain GEMM)
+        self.peer_fuse = self.dense == "packed" and os.environ.get("IG_PEER_FUSE", "1") != "0"
         if self.use_peer:
             try:
                 self.peer_ar = PeerAllReduce(self.B * self.D, group, self.device)
@@ -1153,10 +1169,17 @@ class DecodeEngine:
                 self._mark("attend", li, C, False)
                 self.ev_att[li].record(C)
                 if self.world > 1:
-                    self._gemm(self.attn, self.wo[li], self.o, cs)
-                    if self.peer_ar is not None:                # x_mid = x + sum of partials
+                    if self.peer_ar is not None and self.peer_fuse:
+                        # the GEMM epilogue pushes into every rank; x_mid = x + sum
+                        self.peer_ar.gemm_push(self.attn, self._packed_weight(self.wo[li]), self.D,
+                                               Hg * d, self.st, 2 * li, 2 * L, self.gemm_ws,
+                                               self.gemm_tickets, cs)
+                        self.peer_ar.sum(self.o, x, self.st, 2 * li, 2 * L, cs)
+                    elif self.peer_ar is not None:              # x_mid = x + sum of partials
+                        self._gemm(self.attn, self.wo[li], self.o, cs)
                         self.peer_ar(self.o, self.o, x, self.st, 2 * li, 2 * L, cs)
                     else:
+                        self._gemm(self.attn, self.wo[li], self.o, cs)
                         dist.all_reduce(self.o, group=self.group)
                         self.o.add_(x)                          # x_mid = x + attn_out
                 else:
@@ -1166,10 +1189,16 @@ class DecodeEngine:
                 self._gemm(self.x_f, self.ffn_in[li], self.hidden, cs, epilogue=1)
                 x_new = self.xbuf[1] if x is self.xbuf[0] else self.xbuf[0]
                 if self.Fg != self.F:               # row-parallel FFN-out: sum the ranks
-                    self._gemm(self.hidden, self.ffn_out[li], x_new, cs)
-                    if self.peer_ar is not None:
+                    if self.peer_ar is not None and self.peer_fuse:
+                        self.peer_ar.gemm_push(self.hidden, self._packed_weight(self.ffn_out[li]),
+                                               self.D, self.Fg, self.st, 2 * li + 1, 2 * L,
+                                               self.gemm_ws, self.gemm_tickets, cs)
+                        self.peer_ar.sum(x_new, self.o, self.st, 2 * li + 1, 2 * L, cs)
+                    elif self.peer_ar is not None:
+                        self._gemm(self.hidden, self.ffn_out[li], x_new, cs)
                         self.peer_ar(x_new, x_new, self.o, self.st, 2 * li + 1, 2 * L, cs)
                     else:
+                        self._gemm(self.hidden, self.ffn_out[li], x_new, cs)
                         dist.all_reduce(x_new, group=self.group)
                         x_new.add_(self.o)
                 else:
