@@ -64,6 +64,8 @@ def _args():
     ap.add_argument("--no-resident", dest="resident", action="store_false",
                     help="refetch every selected row each step (the reference's data movement) "
                          "instead of keeping each layer's fetched set resident in HBM")
+    ap.add_argument("--no-spec-stream", dest="spec_stream", action="store_false",
+                    help="run the speculation chain on the compute stream (A/B of the overlap)")
     ap.add_argument("--append-stream", action="store_true",
                     help="run ig_append beside the attention on its own stream (measured neutral)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -259,7 +261,8 @@ def run_b200(a) -> None:
     eng = DecodeEngine(model, cfg, pool_dtype="f16", device=dev, group=group, fetch_ctas=a.fetch_ctas,
                        fetch_threads=a.fetch_threads, fetch_priority=a.fetch_priority,
                        fetch_impl=a.fetch_impl, fetch_rows=a.fetch_rows, dense=a.dense,
-                       cuda_graph=a.cuda_graph, resident=a.resident, append_stream=a.append_stream)
+                       cuda_graph=a.cuda_graph, resident=a.resident, append_stream=a.append_stream,
+                       spec_stream=a.spec_stream)
     # engine holds its own (sharded) copies: drop the full model
     del model
     torch.cuda.empty_cache()

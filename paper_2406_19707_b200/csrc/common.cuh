@@ -5,6 +5,9 @@
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #include "../../include/infinigen_b200.h"
 
@@ -39,6 +42,39 @@ __device__ __forceinline__ float key_to_float(uint32_t k) {
 // after griddepcontrol.wait.  No effect on plainly launched successors.
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Kernels launched with launch_pdl() may start before their predecessor in the
+// stream has finished: they must call pdl_wait() before touching anything the
+// predecessor writes (it returns once that grid has completed and flushed).
+// Only the packed GEMM is launched this way: PDL-launching the layernorm, the
+// append and the attention as well measured 880 vs 957 tok/s (their early CTAs
+// sit on SM slots while they wait and hold off the speculation stream).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("IG_PDL");             // A/B switch: IG_PDL=0 launches plainly
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
+// cudaLaunchKernelEx with programmatic stream serialization (PDL)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 template <typename T>

@@ -463,14 +463,6 @@ inline int grid_for(int N, int K, int cps) {
   return (int)G;
 }
 
-inline bool pdl_enabled() {
-  static const bool v = [] {
-    const char* e = getenv("IG_PDL");             // A/B switch: IG_PDL=0 launches plainly
-    return !(e && atoi(e) == 0);
-  }();
-  return v;
-}
-
 inline int ctas_per_sm(int M) {
   // IG_PACKED_CTA=16: one 16-warp CTA per SM with a 6-deep ring (more bytes in
   // flight, fewer CTA fix-ups) -- measured equal or slower (ffn_out 4.7 vs 5.6
