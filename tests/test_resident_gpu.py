@@ -328,3 +328,23 @@ def test_llama_like_ffn_narrower_than_fused_qkv():
         _cmp_records(eng.records, ref_recs, ocfg.batch, exact=True)
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("batch", [12, 20])
+def test_wide_batch_engine_matches_oracle(batch):
+    """Batches above 8 and above 16 take the packed GEMM's 2-tile (M <= 16) and
+    4-tile (M <= 32, one CTA per SM) paths -- C3 runs B = 16, C5 B = 32: every
+    selection, n and output row still matches the oracle (f32 pool, eviction)."""
+    from paper_2406_19707_b200 import DecodeEngine
+    _, sk = models("m256")
+    ocfg = run_config("spec_counter", batch=batch, gen_len=4, record_selection=True)
+    sessions = oracle_sessions(sk, ocfg)
+    eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg), copy.deepcopy(sessions), pool_dtype="f32")
+    try:
+        ref_out, ref_recs = oracle_decode(sessions, ocfg.gen_len)
+        got = np.stack([eng.x.cpu().numpy()] + [eng.decode_step().cpu().numpy()
+                                                for _ in range(ocfg.gen_len)], axis=1)
+        assert _scaled_err(got, ref_out) < 1e-4
+        _cmp_records(eng.records, ref_recs, ocfg.batch, exact=True)
+    finally:
+        eng.close()
