@@ -13,8 +13,10 @@
 
 namespace ig {
 
-constexpr int kSelThreads = 512;
-constexpr int kSelWarps = kSelThreads / kWarp;
+constexpr int kSelThreads = 512;            // rows up to kSelLongRows keys
+constexpr int kSelThreadsLong = 1024;       // longer rows (C4: 32K): 95 vs 124 us per layer
+constexpr int kSelLongRows = 8192;
+constexpr int kSelWarps = kSelThreadsLong / kWarp;
 constexpr size_t kSelMaxSmem = 220 * 1024;  // keys of rows up to 56K tokens
 
 struct SelShared {
@@ -139,7 +141,8 @@ __device__ void radix_topn(const float* __restrict__ row, int s, int n, int32_t*
   }
 }
 
-__global__ void __launch_bounds__(kSelThreads)
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS)
 select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ count_sum,
               const ig_step_state* __restrict__ st, int Hg, int H_total, int S_max, int cap_max,
               double cap_ratio, int min_select, int32_t* __restrict__ idx,
@@ -213,10 +216,12 @@ extern "C" int ig_select(const float* scores, const int32_t* count_sum, const ig
     return IG_EINVAL;
   const size_t smem = (size_t)S_max * 4;  // the row's order keys
   if (smem > kSelMaxSmem) return IG_EINVAL;
+  auto kern = S_max > kSelLongRows ? select_kernel<kSelThreadsLong> : select_kernel<kSelThreads>;
+  const int threads = S_max > kSelLongRows ? kSelThreadsLong : kSelThreads;
   if (smem > 32 * 1024)  // dynamic + static must fit: opt in early
-    IG_CUDA_STATUS(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    IG_CUDA_STATUS(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
-  select_kernel<<<dim3(Hg, B), kSelThreads, smem, (cudaStream_t)stream>>>(
+  kern<<<dim3(Hg, B), threads, smem, (cudaStream_t)stream>>>(
       scores, count_sum, st, Hg, H_total, S_max, cap_max, cap_ratio, min_select, idx, n_out,
       err_flag);
   IG_LAUNCH_STATUS();
