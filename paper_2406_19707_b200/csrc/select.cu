@@ -17,7 +17,7 @@ constexpr int kSelThreads = 512;            // rows up to kSelLongRows keys
 constexpr int kSelThreadsLong = 1024;       // longer rows (C4: 32K): 95 vs 124 us per layer
 constexpr int kSelLongRows = 8192;
 constexpr int kSelWarps = kSelThreadsLong / kWarp;
-constexpr size_t kSelMaxSmem = 220 * 1024;  // keys of rows up to 56K tokens
+constexpr size_t kSelMaxSmem = 220 * 1024;  // ig_topk_rows: keys of rows up to 56K
 
 struct SelShared {
   uint32_t hist[256];
@@ -141,15 +141,89 @@ __device__ void radix_topn(const float* __restrict__ row, int s, int n, int32_t*
   }
 }
 
+// ---------------------------------------------------------------------------
+// ig_select: value-bin select (one CTA per (b, h) row, the row streamed from
+// L2 -- rehearse_count wrote it just before -- so no shared-memory copy of the
+// keys and no row-length ceiling beyond the 1-bit-per-row take mask).
+//
+//   P0  min / max of the row;
+//   P1  histogram over kBins value bins: bin(x) = min(kBins-1, (hi - x) * scale),
+//       a monotone non-increasing map of the score (IEEE subtraction and
+//       multiplication round monotonically), so every row of a lower bin
+//       outranks every row of a higher bin; a block scan finds the boundary
+//       bin b* holding the n-th largest score and `need`, how many of its rows
+//       are taken;
+//   P2  the rows of b* are gathered (typically a few dozen: kBins bins over the
+//       score range) and ranked exactly by (order key desc, row asc) -- the
+//       reference's stable argsort (linalg.py:184), -0.0 == +0.0 -- and the
+//       taken ones marked in a row bitmap; a boundary bin too full for the
+//       candidate buffer (huge outliers, mass ties) is resolved instead by an
+//       8-bit radix select over the order keys of its rows;
+//   P3  ascending emission with warp ballots / scans, each warp owning one
+//       contiguous row range whose count was taken in P2.
+// ---------------------------------------------------------------------------
+constexpr int kBins = 2048;
+constexpr int kCandMax = 1024;
+constexpr int kSelMaxRows = 1 << 20;        // take bitmap: 128 KB of shared memory
+
+struct BinShared {
+  uint32_t hist[kBins];
+  uint32_t cand_key[kCandMax];
+  int32_t cand_t[kCandMax];
+  uint32_t kmin[kSelWarps], kmax[kSelWarps];
+  int scan[kSelWarps];
+  int warp_a[kSelWarps];      // rows of the warp's range surely taken
+  int warp_b[kSelWarps];      // radix mode: rows of b* whose key == P
+  int bstar, need, m, ncand;
+  SelShared rx;               // radix fallback
+};
+
+__device__ __forceinline__ int vbin(float x, float hi, float scale) {
+  return (int)fminf((hi - x) * scale, (float)(kBins - 1));
+}
+
+// inclusive block scan of one int per thread (warp scans + a scan of warp totals)
+__device__ __forceinline__ int block_incl_scan(int v, int* warp_tot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  if (lane == 31) warp_tot[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) warp_tot[lane] = t;
+  }
+  __syncthreads();
+  const int r = v + (w > 0 ? warp_tot[w - 1] : 0);
+  __syncthreads();
+  return r;
+}
+
+// 4 consecutive scores of a row as a float4 (rows t >= s are masked by callers)
+__device__ __forceinline__ float4 row4(const float* row, int t) {
+  return __ldcg(reinterpret_cast<const float4*>(row + t));
+}
+
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS)
 select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ count_sum,
               const ig_step_state* __restrict__ st, int Hg, int H_total, int S_max, int cap_max,
               double cap_ratio, int min_select, int32_t* __restrict__ idx,
               int32_t* __restrict__ n_out, int32_t* __restrict__ err_flag) {
-  __shared__ SelShared sh;
-  extern __shared__ uint32_t keys[];
+  constexpr int NW = THREADS / kWarp;
+  constexpr int PER = kBins / THREADS;
+  __shared__ BinShared sh;
+  extern __shared__ uint32_t bits[];            // take bitmap, ceil(S_max / 32) words
   const int b = blockIdx.y, h = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int s = st->s_len;
   // n = floor(sum/H + 0.5) == floor((2 sum + H) / 2H) exactly (integers)
   const long long sum = count_sum[b];
@@ -159,12 +233,238 @@ select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ coun
   n = min(n, (long long)s);
   int nn = (int)n;
   if (nn > cap_max) {  // caller sized the index buffer too small: flag and clamp
-    if (threadIdx.x == 0) atomicExch(err_flag, 1);
+    // a plain store (the flag may live in mapped host memory, where device
+    // atomics are not guaranteed): only ever 0 -> 1
+    if (tid == 0) *reinterpret_cast<volatile int32_t*>(err_flag) = 1;
     nn = cap_max;
   }
-  if (h == 0 && threadIdx.x == 0) n_out[b] = nn;
+  if (h == 0 && tid == 0) n_out[b] = nn;
   const size_t bh = (size_t)b * Hg + h;
-  radix_topn(scores + bh * S_max, s, nn, idx + bh * cap_max, sh, keys);
+  const float* row = scores + bh * S_max;
+  int32_t* out = idx + bh * cap_max;
+  if (nn >= s) {
+    for (int t = tid; t < s; t += THREADS) out[t] = t;
+    return;
+  }
+  if (nn <= 0) return;
+
+  // ---- P0: row min / max (order keys)
+  uint32_t kmin = 0xffffffffu, kmax = 0u;
+  for (int t = tid * 4; t < s; t += THREADS * 4) {
+    const float4 v = row4(row, t);
+    const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (t + i < s) {
+        const uint32_t k = order_key(x[i]);
+        kmin = min(kmin, k);
+        kmax = max(kmax, k);
+      }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if (lane == 0) { sh.kmin[w] = kmin; sh.kmax[w] = kmax; }
+  for (int i = tid; i < kBins; i += THREADS) sh.hist[i] = 0;
+  __syncthreads();
+  kmin = sh.kmin[0];
+  kmax = sh.kmax[0];
+  for (int i = 1; i < NW; ++i) { kmin = min(kmin, sh.kmin[i]); kmax = max(kmax, sh.kmax[i]); }
+  const float hi = key_to_float(kmax), lo = key_to_float(kmin);
+  float scale = (float)kBins / (hi - lo);
+  if (!(scale < 1e30f)) scale = 0.f;            // flat (or denormal-range) row: one bin
+
+  // ---- P1: value-bin histogram, boundary bin
+  for (int t = tid * 4; t < s; t += THREADS * 4) {
+    const float4 v = row4(row, t);
+    const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (t + i < s) atomicAdd(&sh.hist[vbin(x[i], hi, scale)], 1u);
+  }
+  __syncthreads();
+  {
+    int c[PER], tot = 0;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) { c[i] = (int)sh.hist[tid * PER + i]; tot += c[i]; }
+    const int incl = block_incl_scan(tot, sh.scan);
+    const int excl = incl - tot;
+    if (excl < nn && incl >= nn) {
+      int cum = excl;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        if (cum + c[i] >= nn) {
+          sh.bstar = tid * PER + i;
+          sh.need = nn - cum;
+          sh.m = c[i];
+          break;
+        }
+        cum += c[i];
+      }
+    }
+    if (tid == 0) sh.ncand = 0;
+  }
+  for (int i = tid; i < (s + 31) / 32; i += THREADS) bits[i] = 0;
+  __syncthreads();
+  const int bstar = sh.bstar, need = sh.need, m = sh.m;
+  // 0: the whole boundary bin is taken; 1: candidates ranked; 2: radix select in b*
+  const int mode = (m == need) ? 0 : (m <= kCandMax ? 1 : 2);
+
+  // warp w owns rows [t_lo, t_hi), a multiple of 128 (its float4 lanes)
+  const int span = ((s + NW - 1) / NW + 127) & ~127;
+  const int t_lo = min(s, w * span), t_hi = min(s, t_lo + span);
+
+  // ---- P2: per-warp counts (+ candidate gather / radix resolve of b*)
+  uint32_t P = 0u;          // radix mode: the key of the need-th largest row in b*
+  int need_eq = 0;          // radix mode: rows with key == P to take (index order)
+  if (mode == 2) {
+    SelShared& rx = sh.rx;
+    uint32_t prefix = 0u, mask = 0u;
+    int nd = need;
+    for (int pass = 0; pass < 4; ++pass) {
+      const int shift = 24 - 8 * pass;
+      for (int i = tid; i < 256; i += THREADS) rx.hist[i] = 0;
+      __syncthreads();
+      for (int t0 = 0; t0 < s; t0 += THREADS) {
+        const int t = t0 + tid;
+        bool live = false;
+        uint32_t bin = 0;
+        if (t < s) {
+          const float x = __ldcg(row + t);
+          const uint32_t key = order_key(x);
+          live = vbin(x, hi, scale) == bstar && (key & mask) == prefix;
+          bin = (key >> shift) & 255u;
+        }
+        const unsigned act = __ballot_sync(0xffffffffu, live);
+        if (live) {
+          const unsigned peers = __match_any_sync(act, bin);
+          if ((__ffs(peers) - 1) == lane) atomicAdd(&rx.hist[bin], (uint32_t)__popc(peers));
+        }
+      }
+      __syncthreads();
+      if (w == 0) pick_digit(rx, prefix, nd, shift);
+      __syncthreads();
+      prefix = rx.prefix;
+      nd = rx.need;
+      mask |= 255u << shift;
+      __syncthreads();
+    }
+    P = prefix;
+    need_eq = nd;
+  }
+  int a = 0, e = 0;
+  for (int t = t_lo + lane * 4; t < t_hi; t += 128) {
+    const float4 v = row4(row, t);
+    const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (t + i >= t_hi) break;
+      const int bn = vbin(x[i], hi, scale);
+      if (bn < bstar) {
+        ++a;
+      } else if (bn == bstar) {
+        if (mode == 0) {
+          ++a;
+        } else if (mode == 1) {
+          const int slot = atomicAdd(&sh.ncand, 1);
+          sh.cand_key[slot] = order_key(x[i]);
+          sh.cand_t[slot] = t + i;
+        } else {
+          const uint32_t k = order_key(x[i]);
+          a += k > P;
+          e += k == P;
+        }
+      }
+    }
+  }
+  a = warp_sum(a);
+  e = warp_sum(e);
+  __syncthreads();
+  if (mode == 1) {
+    // rank the m candidates: (key desc, row asc) -- the reference's stable order
+    for (int i = tid; i < m; i += THREADS) {
+      const uint32_t ki = sh.cand_key[i];
+      const int ti = sh.cand_t[i];
+      int rank = 0;
+      for (int j = 0; j < m; ++j) {
+        const uint32_t kj = sh.cand_key[j];
+        rank += (kj > ki) || (kj == ki && sh.cand_t[j] < ti);
+      }
+      if (rank < need) atomicOr(&bits[ti >> 5], 1u << (ti & 31));
+    }
+    __syncthreads();
+    int tk = 0;     // taken candidates in my range (a is already the warp total)
+    for (int wd = (t_lo >> 5) + lane; wd < (t_hi + 31) >> 5; wd += 32) tk += __popc(bits[wd]);
+    a += warp_sum(tk);
+  }
+  if (lane == 0) { sh.warp_a[w] = a; sh.warp_b[w] = e; }
+  __syncthreads();
+
+  // ---- P3: ascending emission
+  int out_off = 0, eq_before = 0;
+  for (int i = 0; i < w; ++i) {
+    const int ee = min(sh.warp_b[i], max(0, need_eq - eq_before));
+    eq_before += sh.warp_b[i];
+    out_off += sh.warp_a[i] + ee;
+  }
+  for (int t0 = t_lo; t0 < t_hi; t0 += 128) {
+    const int t = t0 + lane * 4;
+    float x[4] = {0.f, 0.f, 0.f, 0.f};
+    if (t < t_hi) {
+      const float4 v = row4(row, t);
+      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+    }
+    bool sure[4], eq[4];
+    int ns = 0, ne = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      sure[i] = eq[i] = false;
+      if (t + i < t_hi) {
+        const int bn = vbin(x[i], hi, scale);
+        if (bn < bstar) {
+          sure[i] = true;
+        } else if (bn == bstar) {
+          if (mode == 0) sure[i] = true;
+          else if (mode == 1) sure[i] = (bits[(t + i) >> 5] >> ((t + i) & 31)) & 1u;
+          else {
+            const uint32_t k = order_key(x[i]);
+            sure[i] = k > P;
+            eq[i] = k == P;
+          }
+        }
+      }
+      ne += eq[i];
+    }
+    // eq rows before this lane (index order), then within the lane
+    int e_incl = ne;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, e_incl, o);
+      if (lane >= o) e_incl += y;
+    }
+    int e_run = eq_before + e_incl - ne;
+    bool take[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      take[i] = sure[i] || (eq[i] && e_run < need_eq);
+      e_run += eq[i];
+      ns += take[i];
+    }
+    int incl = ns;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int pos = out_off + incl - ns;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (take[i]) out[pos++] = t + i;
+    out_off += __shfl_sync(0xffffffffu, incl, 31);
+    eq_before += __shfl_sync(0xffffffffu, e_incl, 31);
+  }
 }
 
 // Rewrite idx[0:n) of each (b, h) into stable descending-score order
@@ -214,11 +514,11 @@ extern "C" int ig_select(const float* scores, const int32_t* count_sum, const ig
       cap_ratio > 1 || min_select < 1 || !scores || !count_sum || !st || !idx || !n_out ||
       !err_flag)
     return IG_EINVAL;
-  const size_t smem = (size_t)S_max * 4;  // the row's order keys
-  if (smem > kSelMaxSmem) return IG_EINVAL;
+  if (S_max > kSelMaxRows) return IG_EINVAL;
+  const size_t smem = (size_t)(S_max + 31) / 32 * 4;  // the take bitmap
   auto kern = S_max > kSelLongRows ? select_kernel<kSelThreadsLong> : select_kernel<kSelThreads>;
   const int threads = S_max > kSelLongRows ? kSelThreadsLong : kSelThreads;
-  if (smem > 32 * 1024)  // dynamic + static must fit: opt in early
+  if (smem > 16 * 1024)  // dynamic + static (~25 KB) must fit: opt in early
     IG_CUDA_STATUS(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
   kern<<<dim3(Hg, B), threads, smem, (cudaStream_t)stream>>>(

@@ -40,6 +40,7 @@ from .speculation import SpeculationConfig, selection_bytes
 from .pool import EvictionPolicy
 
 TRACE_SCHEMA_VERSION = 1
+PACKED_MAX_M = 32          # rows per ig_sgemm_packed launch
 _TORCH_ELT = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}
 
 
@@ -118,40 +119,54 @@ class PeerAllReduce:
     CUDA IPC (handles exchanged once through the process group); one kernel per
     call pushes this rank's partial into every rank, waits for all of them and
     sums in rank order (+ residual).  Replaces the NCCL all-reduce of the W_O /
-    FFN-out partials (engine.py:360-364)."""
+    FFN-out partials (engine.py:360-364).
 
-    def __init__(self, n: int, group, device, dtype=torch.float32):
+    Calls must be numbered densely (seqno = step * calls + call, call in
+    [0, calls)): the receive slots alternate by seqno parity, and a slot is
+    safe to overwrite only because call c + 2 is pushed after the sum of c + 1.
+
+    connect=False allocates locally only; peer_collectives() then exchanges the
+    handles of several objects with one fixed sequence of collectives."""
+
+    def __init__(self, n: int, group, device, dtype=torch.float32, connect: bool = True):
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
-        self.n = n
+        self.n, self.device = n, device
         self.fn = {torch.float32: "ig_allreduce_peer", torch.int32: "ig_allreduce_peer_i32"}[dtype]
+        self.recv = self.flags = None
+        self._opened = []
         recv, flags = ctypes.c_void_p(), ctypes.c_void_p()
         _lib.call("ig_peer_alloc", n, self.world, ctypes.byref(recv), ctypes.byref(flags), kernels=0)
         self.recv, self.flags = recv.value, flags.value
-        self._opened = []
+        self.ticket = self.flags + 4 * 2 * self.world
         try:
             hr, hf = (ctypes.c_char * 64)(), (ctypes.c_char * 64)()
             _lib.call("ig_ipc_get_handle", self.recv, hr, kernels=0)
             _lib.call("ig_ipc_get_handle", self.flags, hf, kernels=0)
-            objs = [None] * self.world
-            dist.all_gather_object(objs, (bytes(hr), bytes(hf)), group=group)
-            pr, pf = [], []
-            for r, (h_r, h_f) in enumerate(objs):
-                if r == self.rank:
-                    pr.append(self.recv)
-                    pf.append(self.flags)
-                    continue
-                for h, lst in ((h_r, pr), (h_f, pf)):
-                    ptr = ctypes.c_void_p()
-                    buf = (ctypes.c_char * 64).from_buffer_copy(h)
-                    _lib.call("ig_ipc_open_handle", buf, ctypes.byref(ptr), kernels=0)
-                    self._opened.append(ptr.value)
-                    lst.append(ptr.value)
-            self.peer_recv = torch.tensor(pr, dtype=torch.int64, device=device)
-            self.peer_flags = torch.tensor(pf, dtype=torch.int64, device=device)
-            self.ticket = self.flags + 4 * 2 * self.world
+            self.handles = (bytes(hr), bytes(hf))
+            if connect:
+                objs = [None] * self.world
+                dist.all_gather_object(objs, self.handles, group=group)
+                self.open(objs)
         except Exception:
             self.close()
             raise
+
+    def open(self, handles) -> None:
+        """Map every other rank's (recv, flags) pair; handles[r] from rank r."""
+        pr, pf = [], []
+        for r, (h_r, h_f) in enumerate(handles):
+            if r == self.rank:
+                pr.append(self.recv)
+                pf.append(self.flags)
+                continue
+            for h, lst in ((h_r, pr), (h_f, pf)):
+                ptr = ctypes.c_void_p()
+                buf = (ctypes.c_char * 64).from_buffer_copy(h)
+                _lib.call("ig_ipc_open_handle", buf, ctypes.byref(ptr), kernels=0)
+                self._opened.append(ptr.value)
+                lst.append(ptr.value)
+        self.peer_recv = torch.tensor(pr, dtype=torch.int64, device=self.device)
+        self.peer_flags = torch.tensor(pf, dtype=torch.int64, device=self.device)
 
     def __call__(self, src, out, residual, st, call: int, calls: int, stream: int) -> None:
         if self.fn == "ig_allreduce_peer_i32":
@@ -177,12 +192,49 @@ class PeerAllReduce:
                   _lib.ptr(residual), out.data_ptr(), stream)
 
     def close(self) -> None:
-        for p in self._opened:
+        for p in getattr(self, "_opened", []):
             _lib.call("ig_ipc_close", p, kernels=0)
         self._opened = []
-        if self.recv:
+        if getattr(self, "recv", None):
             _lib.call("ig_peer_free", self.recv, self.flags, kernels=0)
             self.recv = self.flags = None
+
+
+def _vote(ok: bool, group, device) -> bool:
+    """True iff every rank of the group says ok (one all-reduce)."""
+    t = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                     device=device if dist.get_backend(group) == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return bool(int(t.item()))
+
+
+def peer_collectives(specs, group, device):
+    """PeerAllReduce objects for [(n, dtype), ...], or None on every rank if any
+    rank cannot allocate, export or map them.  Every rank issues the same
+    collectives whatever fails where (vote, gather, vote), so a local failure
+    falls back instead of leaving the ranks in mismatched collectives."""
+    import sys
+    objs, ok = [], True
+    try:
+        for n, dt in specs:
+            objs.append(PeerAllReduce(n, group, device, dt, connect=False))
+    except Exception as e:  # noqa: BLE001 -- no IPC on this box
+        sys.stderr.write(f"peer all-reduce: local setup failed ({e!r})\n")
+        ok = False
+    if _vote(ok, group, device):
+        gathered = [None] * dist.get_world_size(group)
+        dist.all_gather_object(gathered, [o.handles for o in objs], group=group)
+        try:
+            for i, o in enumerate(objs):
+                o.open([g[i] for g in gathered])
+        except Exception as e:  # noqa: BLE001 -- no peer mapping between these GPUs
+            sys.stderr.write(f"peer all-reduce: mapping failed ({e!r})\n")
+            ok = False
+        if _vote(ok, group, device):
+            return objs
+    for o in objs:
+        o.close()
+    return None
 
 
 def _simulate_prefill_rows(n: int, limit: int | None, policy: EvictionPolicy):
@@ -209,6 +261,15 @@ def _simulate_prefill_rows(n: int, limit: int | None, policy: EvictionPolicy):
         arrival[r] = lastf[r] = seq
         ctr[r] = 0
     return row_of, arrival, lastf, ctr, overwrites
+
+
+class SelectionOverflowError(RuntimeError):
+    """A selection larger than the engine's index buffer (flagged by ig_select)."""
+
+
+def _jsonable(rec: dict) -> dict:
+    """A layer record with array fields as lists (schema-v1 JSON)."""
+    return {k: (v.tolist() if isinstance(v, np.ndarray) else v) for k, v in rec.items()}
 
 
 _LAYER_POS = object()     # _attend default: the layer's ig_append positions
@@ -258,7 +319,7 @@ class DecodeEngine:
                  fetch_threads: int = 32, fetch_priority: int = 0, hbm_layers: int = 0,
                  fetch_impl: str = "tma", fetch_rows: int = 16, dense: str = "packed",
                  cuda_graph: bool = False, resident: bool | None = None, spec_stream: bool = True,
-                 append_stream: bool = False):
+                 append_stream: bool = False, shard: tuple[int, int] | None = None):
         config.validate()
         _lib.load()
         _enable_ieee_fp32()
@@ -271,6 +332,15 @@ class DecodeEngine:
         self.group = group
         self.world = dist.get_world_size(group) if group is not None else 1
         self.rank = dist.get_rank(group) if group is not None else 0
+        if shard is not None:
+            # rank r's slice of a G-way head split without a process group: the
+            # per-rank state and kernels only (speculate() hook calls, parity at a
+            # shard's shapes); decode_step / prefill need the group's collectives
+            if group is not None:
+                raise ValueError("shard and group are exclusive")
+            self.rank, self.world = int(shard[0]), int(shard[1])
+            if not 0 <= self.rank < self.world:
+                raise ValueError(f"bad shard {shard}")
         H, D, d, L = spec.heads, spec.model_dim, spec.head_dim, spec.layers
         if H % self.world:
             raise ValueError(f"{H} heads do not shard over {self.world} ranks")
@@ -337,31 +407,22 @@ class DecodeEngine:
         self.peer_ar = self.peer_cnt = None
         # the W_O / FFN-out push folded into the packed GEMM's epilogue (IG_PEER_FUSE=0: a
         # separate push + sum kernel after a plain GEMM)
-        self.peer_fuse = self.dense == "packed" and os.environ.get("IG_PEER_FUSE", "1") != "0"
+        self.peer_fuse = (self.dense == "packed" and self.B <= PACKED_MAX_M
+                          and os.environ.get("IG_PEER_FUSE", "1") != "0")
         if self.use_peer:
-            try:
-                self.peer_ar = PeerAllReduce(self.B * self.D, group, self.device)
-                self.peer_cnt = PeerAllReduce(self.B, group, self.device, torch.int32)
-            except Exception as e:  # noqa: BLE001 -- no IPC / peer access on this box
-                # every rank must take the same path: agree on it through the group
+            pc = peer_collectives([(self.B * self.D, torch.float32), (self.B, torch.int32)],
+                                  group, self.device)
+            if pc is not None:
+                self.peer_ar, self.peer_cnt = pc
+            else:
                 import sys
-                sys.stderr.write(f"DecodeEngine: peer-memory all-reduce unavailable ({e!r}); "
+                sys.stderr.write("DecodeEngine: peer-memory all-reduce unavailable; "
                                  "using the process group\n")
-                for name in ("peer_ar", "peer_cnt"):
-                    if getattr(self, name) is not None:
-                        getattr(self, name).close()
-                        setattr(self, name, None)
-            ok = torch.tensor([1 if self.peer_cnt is not None else 0], dtype=torch.int32,
-                              device=self.device if dist.get_backend(group) == "nccl" else "cpu")
-            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
-            if int(ok.item()) == 0:
-                for name in ("peer_ar", "peer_cnt"):
-                    if getattr(self, name) is not None:
-                        getattr(self, name).close()
-                        setattr(self, name, None)
                 self.use_peer = False
                 if cuda_graph and dist.get_backend(group) != "nccl":
                     raise ValueError("cuda_graph needs NCCL or the peer-memory all-reduce")
+        # dense peer-call numbering per step (PeerAllReduce): W_O (+ FFN-out) per layer
+        self._ar_per_layer = 2 if self.Fg != self.F else 1
         self.s_host = 0
         self._inst = None
         self.iteration = 0
@@ -431,7 +492,12 @@ class DecodeEngine:
         self.count_sum = torch.zeros((L, B), dtype=i32, device=dev)
         self.idx = torch.zeros((L, B, Hg, cap), dtype=i32, device=dev)
         self.n = torch.zeros((L, B), dtype=i32, device=dev)
-        self.err = torch.zeros(1, dtype=i32, device=dev)
+        # device-side error flags in mapped pinned memory, readable by the host at
+        # any time without a sync (graph replays included): [0] = ig_select overflow
+        self._err_mem = HostPool(64)
+        self.err_flags = self._err_mem.numpy(np.int32, (16,))
+        self.err_flags[:] = 0
+        self.err_ptr = self._err_mem.dev
         self.pos = torch.zeros((L, B, Hg), dtype=i32, device=dev)
         self.events = torch.zeros((L, B, Hg, 2), dtype=i64, device=dev)
         self.stage_full = [torch.empty((B, Hg, S, 2 * d), dtype=T, device=dev)
@@ -454,7 +520,8 @@ class DecodeEngine:
             ws = 0
             for N_, K_ in shapes:
                 wf = ctypes.c_size_t()
-                _lib.call("ig_sgemm_packed_sizes", B, N_, K_, None, ctypes.byref(wf), None, kernels=0)
+                _lib.call("ig_sgemm_packed_sizes", min(B, PACKED_MAX_M), N_, K_, None, ctypes.byref(wf),
+                          None, kernels=0)
                 ws = max(ws, wf.value)
             self._pack_weights()
         self.gemm_ws = torch.empty(ws, dtype=f32, device=dev)
@@ -520,6 +587,9 @@ class DecodeEngine:
         st = np.zeros(8, np.int32)
         st[0], st[1] = s_len, limit
         st[2:4] = np.array([seq], np.int64).view(np.int32)
+        # the step counter never goes back: the peer all-reduce epochs (step * calls
+        # + call + 1) must not repeat a value a stale flag may still hold
+        st[4] = int(self.st[4].item())
         self.st.copy_(torch.from_numpy(st))
         self.s_host = s_len
 
@@ -662,6 +732,7 @@ class DecodeEngine:
         tf32=True runs the prefill GEMMs on TF32 tensor cores (bench setup of
         the 13B-class shapes); the default keeps IEEE fp32 like the reference.
         """
+        self._need_group()
         cfg, spec = self.config, self.spec
         L, B, Hg, d, S, D = self.L, self.B, self.Hg, self.d, self.S_max, self.D
         N = cfg.prompt_len
@@ -836,7 +907,7 @@ class DecodeEngine:
         def select():
             _lib.call("ig_select", self.scores.data_ptr(), self.count_sum[li].data_ptr(),
                       self.st.data_ptr(), B, Hg, self.H, S, self.cap, float(sc.cap_ratio),
-                      int(sc.min_select), idx_tmp.data_ptr(), n_tmp.data_ptr(), self.err.data_ptr(), h)
+                      int(sc.min_select), idx_tmp.data_ptr(), n_tmp.data_ptr(), self.err_ptr, h)
 
         def attend():
             if self.resident:
@@ -858,6 +929,76 @@ class DecodeEngine:
             ms = best(fn)
             out[name] = {"ms": ms, "bytes": nbytes, "gbs": nbytes / (ms * 1e6)}
         torch.cuda.synchronize(self.device)
+        return out
+
+    def check_errors(self) -> None:
+        """Raise for a device-side error flagged by any step launched so far whose
+        flag write has reached the host (call after a synchronize to cover all
+        of them).  decode_step polls this before every step, graph replays too."""
+        if self.err_flags[0]:
+            self.err_flags[0] = 0
+            raise SelectionOverflowError("selection exceeded the index buffer (cap): n > "
+                                         f"{self.cap} rows for some sequence")
+
+    def _need_group(self) -> None:
+        if self.world > 1 and self.group is None:
+            raise ValueError("a shard engine without a process group runs speculate() only")
+
+    @torch.no_grad()
+    def speculate(self, li: int, x_a=None, qspec=None, extra_counts=None) -> dict:
+        """The product speculation chain for layer ``li`` (run at layer li-1 in
+        decode_step) as one hook call on the engine's current state: the fused
+        packed GEMM x_a(li-1) . [W_QKV(li-1) | W_Q(li)] -> ig_rehearse_count(li)
+        -> ig_select(li) -- the launches _step makes, on the compute stream.
+
+        x_a : [B, D] LN1 output of layer li-1 (the reference speculate_scores'
+            x_a_prev, engine.py:311-316); default: the engine's x_a buffer.
+        qspec : optional [B, Hg, k] partial queries replayed in place of the
+            GEMM's (x_a . partial_w_q, speculation.py:133), so the rehearsal and
+            selection kernels are checked on identical inputs.
+        extra_counts : optional [B] int head counts of the heads other ranks
+            own (what the count all-reduce adds on a shard engine).
+
+        Returns host arrays: scores [B, Hg, s], counts [B, Hg], count_sum [B],
+        n [B], idx [B, Hg, cap] (ascending, first n valid).  Decode state
+        (pool, partial keys, selections, slot tables) is not modified."""
+        if self.scheme != "speculative" or not (1 <= li < self.L):
+            raise ValueError("speculate needs the speculative scheme and 1 <= layer < L")
+        B, Hg, d, S, kc = self.B, self.Hg, self.d, self.S_max, self.kcols
+        sc = self.config.speculation
+        s = self.s_host
+        C = self.compute
+        C.wait_stream(torch.cuda.current_stream(self.device))
+        cs = C.cuda_stream
+        with torch.cuda.stream(C):
+            if qspec is None:
+                if x_a is not None:
+                    self.x_a.copy_(_f32(x_a, self.device).reshape(B, self.D))
+                self._gemm(self.x_a, self.wfused[li - 1], self.qkvq, cs)
+                q_ptr, ldq, cols, dq = self.qspec.data_ptr(), self.qkvq.stride(0), self.cols[li], d
+            else:
+                q = _f32(qspec, self.device).reshape(B, Hg * kc)
+                q_ptr, ldq, dq = q.data_ptr(), Hg * kc, kc
+                cols = torch.arange(kc, dtype=torch.int32, device=self.device).repeat(B, Hg, 1).contiguous()
+            csum = torch.zeros(B, dtype=torch.int32, device=self.device)
+            counts = torch.zeros((B, Hg), dtype=torch.int32, device=self.device)
+            _lib.call("ig_rehearse_count", q_ptr, ldq, cols.data_ptr(), self.pk[li - 1].data_ptr(),
+                      self.st.data_ptr(), B, Hg, dq, kc, S, self.scale, float(sc.alpha),
+                      self.scores.data_ptr(), self.maxkey.data_ptr(), self.rtickets.data_ptr(),
+                      counts.data_ptr(), csum.data_ptr(), cs)
+            if extra_counts is not None:
+                csum += torch.as_tensor(np.asarray(extra_counts, np.int32), device=self.device)
+            idx = torch.zeros((B, Hg, self.cap), dtype=torch.int32, device=self.device)
+            n = torch.zeros(B, dtype=torch.int32, device=self.device)
+            err = torch.zeros(1, dtype=torch.int32, device=self.device)
+            _lib.call("ig_select", self.scores.data_ptr(), csum.data_ptr(), self.st.data_ptr(), B, Hg,
+                      self.H, S, self.cap, float(sc.cap_ratio), int(sc.min_select), idx.data_ptr(),
+                      n.data_ptr(), err.data_ptr(), cs)
+            out = {"scores": self.scores[:, :, :s].cpu().numpy(), "counts": counts.cpu().numpy(),
+                   "count_sum": csum.cpu().numpy(), "n": n.cpu().numpy(), "idx": idx.cpu().numpy()}
+        torch.cuda.current_stream(self.device).wait_stream(C)
+        if int(err.item()):
+            raise RuntimeError("selection exceeded the index buffer (cap)")
         return out
 
     # ----------------------------------------------------------------- decode
@@ -900,10 +1041,15 @@ class DecodeEngine:
             P = self._packed_weight(W)
             if self._inst is not None:
                 self._mark("dense", -1, self.compute, True, 4 * (K * N + M * K + M * N))
-            _lib.call("ig_sgemm_packed", X.data_ptr(), X.stride(0), P.data_ptr(), N, K, Y.data_ptr(),
-                      Y.stride(0), _lib.ptr(R), R.stride(0) if R is not None else 0, M, epilogue,
-                      self.gemm_ws.data_ptr(), self.gemm_ws.numel(), self.gemm_tickets.data_ptr(),
-                      self.gemm_tickets.numel(), cs)
+            # the packed kernel takes <= 32 rows (its x fragments); larger batches
+            # stream the weights once per 32-row chunk
+            for m0 in range(0, M, PACKED_MAX_M):
+                m = min(PACKED_MAX_M, M - m0)
+                _lib.call("ig_sgemm_packed", X[m0:].data_ptr(), X.stride(0), P.data_ptr(), N, K,
+                          Y[m0:].data_ptr(), Y.stride(0), _lib.ptr(R[m0:] if R is not None else None),
+                          R.stride(0) if R is not None else 0, m, epilogue, self.gemm_ws.data_ptr(),
+                          self.gemm_ws.numel(), self.gemm_tickets.data_ptr(),
+                          self.gemm_tickets.numel(), cs)
             if self._inst is not None:
                 self._mark("dense", -1, self.compute, False)
             return
@@ -964,6 +1110,8 @@ class DecodeEngine:
         device (an engine buffer: valid until the next decode_step)."""
         if self.s_host < 1:
             raise RuntimeError("prefill has not run")
+        self._need_group()
+        self.check_errors()
         if self.config.pool_limit is None and self.s_host >= self.S_max:
             # the reference grows its pool without bound; this one was sized at
             # construction (prompt_len + max_steps rows) and must not overrun
@@ -1022,6 +1170,7 @@ class DecodeEngine:
         aps = AP.cuda_stream
         recs = [[None] * L for _ in range(B)]
         spec_scores = [None] * L
+        nar = self._ar_per_layer
         C.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(C):
             self.count_sum.zero_()
@@ -1077,7 +1226,7 @@ class DecodeEngine:
                         self._mark("select", nxt, SP, True)
                         if self.peer_cnt is not None:
                             self.peer_cnt(self.count_sum[nxt], self.count_sum[nxt], None, self.st,
-                                          nxt, L, sps)
+                                          nxt - 1, L - 1, sps)
                         elif self.world > 1:
                             with torch.cuda.stream(SP):
                                 dist.all_reduce(self.count_sum[nxt], group=self.group)
@@ -1085,7 +1234,7 @@ class DecodeEngine:
                                   self.count_sum[nxt].data_ptr(), self.st.data_ptr(), B, Hg,
                                   self.H, self.S_max, self.cap, float(sc.cap_ratio),
                                   int(sc.min_select), self.idx[nxt].data_ptr(),
-                                  self.n[nxt].data_ptr(), self.err.data_ptr(), sps)
+                                  self.n[nxt].data_ptr(), self.err_ptr, sps)
                         self._mark("select", nxt, SP, False)
                         if cfg.record_scores:
                             spec_scores[nxt] = self.scores[:, :, :s].cpu()
@@ -1172,12 +1321,12 @@ class DecodeEngine:
                     if self.peer_ar is not None and self.peer_fuse:
                         # the GEMM epilogue pushes into every rank; x_mid = x + sum
                         self.peer_ar.gemm_push(self.attn, self._packed_weight(self.wo[li]), self.D,
-                                               Hg * d, self.st, 2 * li, 2 * L, self.gemm_ws,
+                                               Hg * d, self.st, nar * li, nar * L, self.gemm_ws,
                                                self.gemm_tickets, cs)
-                        self.peer_ar.sum(self.o, x, self.st, 2 * li, 2 * L, cs)
+                        self.peer_ar.sum(self.o, x, self.st, nar * li, nar * L, cs)
                     elif self.peer_ar is not None:              # x_mid = x + sum of partials
                         self._gemm(self.attn, self.wo[li], self.o, cs)
-                        self.peer_ar(self.o, self.o, x, self.st, 2 * li, 2 * L, cs)
+                        self.peer_ar(self.o, self.o, x, self.st, nar * li, nar * L, cs)
                     else:
                         self._gemm(self.attn, self.wo[li], self.o, cs)
                         dist.all_reduce(self.o, group=self.group)
@@ -1191,12 +1340,12 @@ class DecodeEngine:
                 if self.Fg != self.F:               # row-parallel FFN-out: sum the ranks
                     if self.peer_ar is not None and self.peer_fuse:
                         self.peer_ar.gemm_push(self.hidden, self._packed_weight(self.ffn_out[li]),
-                                               self.D, self.Fg, self.st, 2 * li + 1, 2 * L,
+                                               self.D, self.Fg, self.st, nar * li + 1, nar * L,
                                                self.gemm_ws, self.gemm_tickets, cs)
-                        self.peer_ar.sum(x_new, self.o, self.st, 2 * li + 1, 2 * L, cs)
+                        self.peer_ar.sum(x_new, self.o, self.st, nar * li + 1, nar * L, cs)
                     elif self.peer_ar is not None:
                         self._gemm(self.hidden, self.ffn_out[li], x_new, cs)
-                        self.peer_ar(x_new, x_new, self.o, self.st, 2 * li + 1, 2 * L, cs)
+                        self.peer_ar(x_new, x_new, self.o, self.st, nar * li + 1, nar * L, cs)
                     else:
                         self._gemm(self.hidden, self.ffn_out[li], x_new, cs)
                         dist.all_reduce(x_new, group=self.group)
@@ -1236,8 +1385,8 @@ class DecodeEngine:
             self._res_valid = True
         torch.cuda.current_stream(self.device).wait_stream(C)
         self.s_host = s_next
-        if speculative and L > 1 and int(self.err.item() if recording else 0):
-            raise RuntimeError("selection exceeded the index buffer (cap)")
+        if recording:
+            self.check_errors()
         if recording:
             self.records.append([recs[b] for b in range(B)])
         self.iteration += 1
@@ -1277,8 +1426,7 @@ class DecodeEngine:
                     sel.append(sorted(int(i) for i in rows if i != pos[b, h]))
                 r["selected"] = sel
             if cfg.record_scores and speculative and li >= 1 and spec_scores[li] is not None:
-                r["spec_scores"] = [[float(v) for v in spec_scores[li][b, h].tolist()]
-                                    for h in range(self.Hg)]
+                r["spec_scores"] = spec_scores[li][b].numpy()     # [Hg, s]; lists in trace()
             recs[b][li] = r
 
     def step_host(self, x_host: np.ndarray | None = None) -> np.ndarray:
@@ -1287,7 +1435,9 @@ class DecodeEngine:
         if x_host is not None:
             self.x.copy_(torch.from_numpy(np.ascontiguousarray(x_host, np.float32)).reshape(self.B, self.D),
                          non_blocking=True)
-        return self.decode_step().cpu().numpy()
+        out = self.decode_step().cpu().numpy()
+        self.check_errors()
+        return out
 
     def trace(self) -> dict:
         """Schema-v1 trace (engine.py:83-196; selected lists are ascending)."""
@@ -1303,11 +1453,12 @@ class DecodeEngine:
                            "prompt_seed": cfg.prompt_seed,
                            "kv_bytes_per_element": cfg.kv_bytes_per_element},
                 "sequences": [{"prefill": dict(self.prefill_info),
-                               "iterations": [it[b] for it in self.records]}
+                               "iterations": [[_jsonable(r) for r in it[b]] for it in self.records]}
                               for b in range(self.B)]}
 
     def close(self) -> None:
         self.pool.close()
+        self._err_mem.close()
         for name in ("peer_ar", "peer_cnt"):
             if getattr(self, name, None) is not None:
                 getattr(self, name).close()

@@ -140,8 +140,32 @@ def speculate_scores(x_a_prev, artifacts, layer: int, head_dim: int) -> list:
     pwq = torch.from_numpy(np.concatenate([np.asarray(a.partial_w_q, np.float32) for a in arts], axis=1)).to(dev)
     pk = torch.zeros((1, H, k, S), dtype=torch.float32, device=dev)
     pk[0, :, :, :s] = torch.from_numpy(np.stack([np.asarray(a.partial_k, np.float32).T for a in arts])).to(dev)
-    torch.backends.cuda.matmul.allow_tf32 = False
-    qpart = (x @ pwq).contiguous()                         # [1, H*k]: the partial queries
+    # the partial queries x . partial_w_q (speculation.py:133), accumulated in f64 and
+    # rounded once: within an ulp of any f32 summation order of the reference's sgemv
+    qpart = (x.double() @ pwq.double()).float().contiguous()      # [1, H*k]
+    return _rehearse(torch, qpart, pk, s, k, head_dim)
+
+
+def rehearse_partial_queries(qpart, artifacts, layer: int, head_dim: int) -> list:
+    """The second half of speculate_scores on given partial queries
+    (qpart [H, k] = x . partial_w_q per head): parity tests replay the
+    reference's own queries through the rehearsal kernel with this."""
+    torch = _torch()
+    dev = torch.device("cuda")
+    H = artifacts.heads
+    arts = [artifacts.head(layer, h) for h in range(H)]
+    s, k = arts[0].partial_k.shape
+    S = (s + 3) // 4 * 4
+    pk = torch.zeros((1, H, k, S), dtype=torch.float32, device=dev)
+    pk[0, :, :, :s] = torch.from_numpy(np.stack([np.asarray(a.partial_k, np.float32).T for a in arts])).to(dev)
+    q = torch.from_numpy(np.ascontiguousarray(qpart, dtype=np.float32).reshape(1, H * k)).to(dev)
+    return _rehearse(torch, q, pk, s, k, head_dim)
+
+
+def _rehearse(torch, qpart, pk, s: int, k: int, head_dim: int) -> list:
+    dev = qpart.device
+    H = pk.shape[1]
+    S = pk.shape[3]
     cols = torch.arange(k, dtype=torch.int32, device=dev).repeat(1, H, 1).contiguous()
     scores = torch.empty((1, H, S), dtype=torch.float32, device=dev)
     maxkey = torch.zeros((1, H), dtype=torch.int32, device=dev)

@@ -62,6 +62,63 @@ def test_select_tokens_random_with_ties(seed):
             np.testing.assert_array_equal(got_p[h], ref_p[h])
 
 
+def _select_direct(sc: np.ndarray, cfg):
+    """ig_select on [H, s] scores with the reference's head counts: (n, [H] ascending rows)."""
+    import math
+    import torch
+    from paper_2406_19707_b200 import _lib
+    H, s = sc.shape
+    S = (s + 3) // 4 * 4
+    dsc = torch.zeros((1, H, S), dtype=torch.float32, device="cuda")
+    dsc[0, :, :s] = torch.from_numpy(sc).cuda()
+    counts = [int(np.sum(v > np.float32(float(np.max(v)) - cfg.alpha))) for v in sc]
+    csum = torch.tensor([sum(counts)], dtype=torch.int32, device="cuda")
+    st = torch.zeros(8, dtype=torch.int32, device="cuda")
+    st[0] = s
+    cap = max(int(math.floor(cfg.cap_ratio * s)), cfg.min_select, 1)
+    idx = torch.full((1, H, cap), -7, dtype=torch.int32, device="cuda")
+    n = torch.zeros(1, dtype=torch.int32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.call("ig_select", dsc.data_ptr(), csum.data_ptr(), st.data_ptr(), 1, H, H, S, cap,
+              float(cfg.cap_ratio), int(cfg.min_select), idx.data_ptr(), n.data_ptr(), err.data_ptr(),
+              _lib.stream_handle())
+    assert int(err.item()) == 0
+    nn = int(n.item())
+    got = idx[0].cpu().numpy()
+    assert (got[:, nn:] == -7).all()            # nothing written past n
+    return nn, [got[h, :nn] for h in range(H)]
+
+
+@pytest.mark.parametrize("s", [4096, 8193, 32768, 65536, 131072])
+@pytest.mark.parametrize("kind", ["normal", "outlier", "flat", "ties", "zeros"])
+def test_select_long_rows_and_adversarial(s, kind):
+    """ig_select (value bins -> exact rank of the boundary bin, or a radix select
+    inside it when it overflows the candidate buffer) vs the reference's stable
+    argsort at long contexts (no row-length ceiling below 1M): a huge outlier
+    squeezes every other score into one bin (radix path), a flat row is one bin,
+    rounded scores tie massively, and +-0.0 tie with each other."""
+    rng = np.random.default_rng(s + len(kind))
+    H = 3
+    sc = rng.standard_normal((H, s)).astype(np.float32) * np.float32(2.5)
+    if kind == "outlier":
+        sc[:, rng.integers(0, s, 2)] = np.float32(1e6)
+        sc[1, 5] = np.float32(-1e7)
+    elif kind == "flat":
+        sc[:] = np.float32(0.75)
+    elif kind == "ties":
+        sc = np.round(sc).astype(np.float32)
+    elif kind == "zeros":
+        sc[:, ::3] = 0.0
+        sc[:, 1::3] = -0.0
+    for alpha, cap_ratio in ((4.0, 0.2), (1e9, 0.05), (0.5, 1.0)):
+        cfg = O.SpeculationConfig(0.3, alpha, cap_ratio, 1)
+        ref_p, ref_n = O.select_tokens([sc[h] for h in range(H)], cfg)
+        n, got = _select_direct(sc, cfg)
+        assert n == ref_n, (kind, alpha)
+        for h in range(H):
+            np.testing.assert_array_equal(got[h], np.sort(ref_p[h]))
+
+
 def test_topk_rows_matches_stable_argsort():
     import torch
     from paper_2406_19707_b200 import _lib

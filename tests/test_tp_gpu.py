@@ -14,7 +14,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, ffn=None):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -22,11 +22,16 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle import speckv_port as O
-        from tests.golden_cfg import models, run_config
+        from tests.golden_cfg import MODELS, models, run_config
         from tests.test_engine_gpu import engine_cfg, oracle_sessions, oracle_decode
         from paper_2406_19707_b200 import DecodeEngine
         torch.cuda.set_device(0)
-        _, sk = models("m64")
+        if ffn is None:
+            _, sk = models("m64")
+        else:       # an FFN width that does not shard (replicated FFN, one all-reduce per layer)
+            import dataclasses
+            sk = O.skew_model(O.generate_synthetic(dataclasses.replace(MODELS["m64"], ffn_dim=ffn)),
+                              calib_seed=0)
         for rname in ("spec", "spec_counter"):
             ocfg = run_config(rname, record_selection=True)
             sessions = oracle_sessions(sk, ocfg)
@@ -46,18 +51,22 @@ def _worker(rank, world, port, q):
                             mism += set(sel) != set(rr["selected"][eng.h0 + hl])
             peer = eng.peer_ar is not None
             eng.close()
-            q.put((rank, rname, err, mism, (eng.Hg, peer)))
+            q.put((rank, rname, err, mism, (eng.Hg, peer, eng.Fg == eng.F)))
     except Exception as e:  # surface the failure to the parent
         q.put((rank, "error", repr(e), -1, 0))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("peer", ["1", "0"])
-def test_two_rank_head_parallel_matches_oracle(peer, monkeypatch):
+@pytest.mark.parametrize("world,peer,ffn", [(2, "1", None), (2, "0", None), (4, "1", None),
+                                            (2, "1", 260), (4, "1", 260)])
+def test_head_parallel_matches_oracle(world, peer, ffn, monkeypatch):
     """peer = 1 (default): the W_O / FFN-out all-reduces run over peer memory
-    (ig_allreduce_peer, buffers mapped by CUDA IPC between the two processes);
-    peer = 0: through the process group (gloo here, NCCL on a multi-GPU box)."""
+    (ig_allreduce_peer, buffers mapped by CUDA IPC between the processes);
+    peer = 0: through the process group (gloo here, NCCL on a multi-GPU box).
+    world = 4 (one head per rank) exercises the G > 2 flag / slot logic;
+    ffn = 260 does not split into 16-B shards, so the FFN is replicated and
+    the step has one output all-reduce per layer (dense call numbering)."""
     monkeypatch.setenv("IG_PEER_AR", peer)
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
@@ -66,15 +75,15 @@ def test_two_rank_head_parallel_matches_oracle(peer, monkeypatch):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 31000 + int.from_bytes(os.urandom(2), "little") % 2000
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, ffn)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=600) for _ in range(4)]
+    res = [q.get(timeout=900) for _ in range(2 * world)]
     for p in procs:
         p.join(timeout=120)
     for rank, rname, err, mism, info in res:
         assert rname != "error", err
-        assert info == (2, peer == "1")
+        assert info == (4 // world, peer == "1", ffn is not None)
         assert err < 1e-4, (rank, rname, err)
         assert mism == 0, (rank, rname, mism)
 
