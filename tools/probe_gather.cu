@@ -106,25 +106,5 @@ int main() {
       }
     }
   }
-  // copy engine: one memcpy per row, batched via cudaMemcpyBatchAsync when available
-#if CUDART_VERSION >= 12080
-  {
-    int n = 65536;
-    std::vector<void*> dsts(n), srcs(n); std::vector<size_t> sizes(n, 512);
-    for (int i = 0; i < n; ++i) { dsts[i] = d + (size_t)i * 512; srcs[i] = h + (size_t)rows[i] * 512; }
-    cudaMemcpyAttributes attr = {}; attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.srcLocHint.type = cudaMemLocationTypeHost; attr.dstLocHint.type = cudaMemLocationTypeDevice;
-    size_t attrIdx = 0, fail = 0;
-    cudaStream_t s; cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
-    cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &attrIdx, 1, &fail, s);
-    if (e == cudaSuccess) {
-      cudaStreamSynchronize(s);
-      cudaEventRecord(a, s);
-      cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr, &attrIdx, 1, &fail, s);
-      cudaEventRecord(b, s); cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
-      printf("{\"variant\":\"ce_batch_512B\",\"copies\":%d,\"gbs\":%.2f}\n", n, (double)n * 512 / ms / 1e6);
-    } else printf("{\"variant\":\"ce_batch_512B\",\"error\":\"%s\"}\n", cudaGetErrorString(e));
-  }
-#endif
   return 0;
 }
