@@ -263,15 +263,19 @@ def run_b200(a) -> None:
                        fetch_impl=a.fetch_impl, fetch_rows=a.fetch_rows, dense=a.dense,
                        cuda_graph=a.cuda_graph, resident=a.resident, append_stream=a.append_stream,
                        spec_stream=a.spec_stream)
-    # engine holds its own (sharded) copies: drop the full model
-    del model
+    del model               # the engine holds the only reference until the prefill is done
     torch.cuda.empty_cache()
     g = torch.Generator(device=dev)
     g.manual_seed(1234)
     prompts = torch.empty(a.batch, a.prompt, spec.model_dim, device=dev).normal_(generator=g)
-    eng.prefill(prompts, tf32=True)
+    t_pf = time.time()
+    eng.prefill(prompts)
+    prefill_s = time.time() - t_pf
     del prompts
+    if a.dense == "packed":
+        eng.release_model()  # decode reads only the packed weights: one copy in HBM
     torch.cuda.empty_cache()
+    footprint = eng.hbm_footprint()
     setup_s = time.time() - t_setup
 
     def barrier():
@@ -446,7 +450,9 @@ def run_b200(a) -> None:
                 "e2e": {"value": tok / (e2e_ms / 1000.0), "unit": UNIT,
                         "h2d_bytes_per_step": a.batch * spec.model_dim * 4,
                         "d2h_bytes_per_step": a.batch * spec.model_dim * 4},
-                "gpu_launches": launches, "setup_s": setup_s,
+                "gpu_launches": launches, "setup_s": setup_s, "prefill_s": prefill_s,
+                "hbm_footprint_gb": {k: (v / 1e9 if isinstance(v, int) else v)
+                                     for k, v in footprint.items()},
                 "link_bytes_per_step": {"reference_accounted": _ref_bytes(stats, eng, a.steps),
                                         "moved": f_bytes / a.steps}}
         if var_stats is not None and var_kind == "refetch":

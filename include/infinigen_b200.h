@@ -298,6 +298,22 @@ int ig_step_advance(ig_step_state* st, void* stream);
 int ig_layernorm(const float* x, const float* gain, const float* bias, float eps,
                  int rows, int D, float* out, void* stream);
 
+/* ---- prefill projections on tcgen05 -------------
+ * The prompt-length GEMMs of DecodeSession._prefill / forward_block
+ * (engine.py:245-291, model.py:195-244: x_a @ W_QKV, attn @ W_O, the FFN) at
+ * f32-level accuracy on the 5th-generation tensor cores.  Operands are split
+ * once into f16 hi/lo pairs with a power-of-two scale per operand row
+ * (ig_split_f16: out [rows][2 Kp] f16 = hi in [0, Kp), lo in [Kp, 2 Kp),
+ * Kp = K rounded up to 64; transpose = 1 takes W [K][N] and emits W^T rows),
+ * then ig_gemm_tc05 computes C = A @ W (+ ReLU, epilogue 1 / + R, epilogue 2)
+ * as hi.hi + hi.lo + lo.hi accumulated in f32 in TMEM (tcgen05.mma kind::f16,
+ * TMA-fed 128-B-swizzled tiles).  max_ctas <= 0: one CTA per SM. */
+int ig_split_f16(const float* X, int ldx, int rows, int cols, int transpose, int Kp, void* out,
+                 float* inv_scale, void* stream);
+int ig_gemm_tc05(const void* A_hl, const float* inv_sa, const void* B_hl, const float* inv_sb, int M,
+                 int N, int K, int Kp, float* C, int ldc, const float* R, int ldr, int epilogue,
+                 int max_ctas, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

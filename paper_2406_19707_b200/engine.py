@@ -88,6 +88,40 @@ def _enable_ieee_fp32():
         pass
 
 
+class _Weight:
+    """One decode-step weight matrix [K, N] of this rank: its row-major f32 copy
+    (dense paths "ig" / "tc" / "cublas") or its ig_sgemm_packed blocks
+    (dense="packed": the row-major copy is dropped once packed)."""
+
+    def __init__(self, rm: torch.Tensor | None, packed: bool, device, *, _shape=None):
+        self.is_view = rm is None
+        self.K, self.N = (rm.shape if rm is not None else _shape)
+        self.rm = None if packed else rm
+        self.packed = None
+        if packed and rm is not None:
+            K, N = rm.shape
+            pf = ctypes.c_size_t()
+            _lib.call("ig_sgemm_packed_sizes", 1, N, K, ctypes.byref(pf), None, None, kernels=0)
+            self.packed = torch.empty(pf.value, dtype=torch.float32, device=device)
+            _lib.call("ig_sgemm_pack", rm.data_ptr(), rm.stride(0), N, K, self.packed.data_ptr(),
+                      torch.cuda.current_stream(device).cuda_stream, kernels=2)
+
+    @property
+    def shape(self):
+        return (self.K, self.N)
+
+    def narrow(self, n: int) -> "_Weight":
+        """The first n columns (the q/k/v part of the fused [QKV | Q(li+1)]
+        matrix): a row-major view; packed blocks are not sliceable."""
+        w = _Weight(None, False, None, _shape=(self.K, n))
+        w.rm = self.rm[:, :n] if self.rm is not None else None
+        return w
+
+    def nbytes(self) -> int:
+        t = self.packed if self.packed is not None else self.rm
+        return 0 if t is None else t.numel() * t.element_size()
+
+
 class HostPool:
     """Pinned, mapped, portable host memory for the KV rows (ig_host_alloc)."""
 
@@ -400,6 +434,9 @@ class DecodeEngine:
         self._res_valid = False
         self.spec_stream_on = bool(spec_stream)
         self.append_stream_on = bool(append_stream)
+        # IG_APPEND_FIRST=1: launch ig_append(li) before releasing the speculation
+        # chain of li+1 (measured at C3: 952 vs 984 tok/s -- off)
+        self.append_first = os.environ.get("IG_APPEND_FIRST", "0") == "1"
         self.scale = float(np.float32(1.0 / np.sqrt(d)))   # speculation.py:127
         self._load_weights(model)
         self._alloc()
@@ -432,31 +469,92 @@ class DecodeEngine:
         self._res_valid = False
 
     # ------------------------------------------------------------------ setup
-    def _load_weights(self, model) -> None:
+    def _layer_rowmajor(self, li: int, model=None) -> dict:
+        """Row-major f32 weights of layer li over this rank's heads / FFN slice
+        (views of the model's tensors where no slicing copy is needed)."""
+        model = self.model if model is None else model
+        if model is None:
+            raise RuntimeError("the engine's model was released (release_model); "
+                               "row-major weights are gone")
         dev, d, Hg, h0 = self.device, self.d, self.Hg, self.h0
         c0, c1 = h0 * d, (h0 + Hg) * d
+        layers = model.layers
+        lw = layers[li]
+        q, k, v = (_f32(getattr(lw, f), dev) for f in ("w_q", "w_k", "w_v"))
+        parts = [q[:, c0:c1], k[:, c0:c1], v[:, c0:c1]]
+        if self.scheme == "speculative" and li + 1 < len(layers):
+            parts.append(_f32(layers[li + 1].w_q, dev)[:, c0:c1])
+        f0, f1 = self.f0, self.f0 + self.Fg
+        return {"qkvq": torch.cat(parts, dim=1).contiguous(),
+                "wo": _f32(lw.w_o, dev)[c0:c1].contiguous(),
+                "ffn_in": _f32(lw.ffn_in, dev)[:, f0:f1].contiguous(),
+                "ffn_out": _f32(lw.ffn_out, dev)[f0:f1].contiguous()}
+
+    def _load_weights(self, model) -> None:
+        """Per layer: [W_Q | W_K | W_V](li) | W_Q(li+1) over this rank's heads
+        (the projections of layer li and the speculation query of layer li+1
+        read the same input x_a(li), engine.py:311-327 / speculation.py:133, so
+        one GEMM launch streams both), W_O rows, FFN slices, LN vectors.
+
+        dense="packed": each matrix is packed (ig_sgemm_pack) as soon as its
+        row-major copy is built and that copy is dropped, so HBM holds ONE copy
+        of the decode weights; the prefill re-derives row-major layers from the
+        model (self.model) one layer at a time."""
+        dev = self.device
         self.wqkv, self.wo, self.ffn_in, self.ffn_out, self.ln = [], [], [], [], []
-        # wfused[li] = [W_Q | W_K | W_V](li) | W_Q(li+1) over this rank's heads: the
-        # projections of layer li and the speculation query of layer li+1 read the
-        # same input x_a(li) (engine.py:311-327 / speculation.py:133), so one
-        # GEMM launch streams both (W_Q(li+1) is stored twice); wqkv[li] is a view.
         self.wfused = []
-        layers = list(model.layers)
-        spec_ = getattr(self.config.scheme, "value", self.config.scheme) == "speculative"
-        for li, lw in enumerate(layers):
-            q, k, v = (_f32(getattr(lw, f), dev) for f in ("w_q", "w_k", "w_v"))
-            parts = [q[:, c0:c1], k[:, c0:c1], v[:, c0:c1]]
-            if spec_ and li + 1 < len(layers):
-                parts.append(_f32(layers[li + 1].w_q, dev)[:, c0:c1])
-            wf = torch.cat(parts, dim=1).contiguous()
-            self.wfused.append(wf if len(parts) == 4 else None)
-            self.wqkv.append(wf[:, :3 * (c1 - c0)])
-            self.wo.append(_f32(lw.w_o, dev)[c0:c1].contiguous())
-            f0, f1 = self.f0, self.f0 + self.Fg
-            self.ffn_in.append(_f32(lw.ffn_in, dev)[:, f0:f1].contiguous())
-            self.ffn_out.append(_f32(lw.ffn_out, dev)[f0:f1].contiguous())
+        Hgd = self.Hg * self.d
+        packed = self.dense == "packed"
+        for li, lw in enumerate(model.layers):
+            rm = self._layer_rowmajor(li, model)
+            fused = rm["qkvq"].shape[1] == 4 * Hgd
+            wf = _Weight(rm["qkvq"], packed, self.device)
+            self.wfused.append(wf if fused else None)
+            self.wqkv.append(wf.narrow(3 * Hgd) if fused else wf)
+            self.wo.append(_Weight(rm["wo"], packed, dev))
+            self.ffn_in.append(_Weight(rm["ffn_in"], packed, dev))
+            self.ffn_out.append(_Weight(rm["ffn_out"], packed, dev))
+            del rm
             self.ln.append(tuple(_f32(getattr(lw, f), dev) for f in
                                  ("ln1_gain", "ln1_bias", "ln2_gain", "ln2_bias")))
+        if packed:
+            torch.cuda.synchronize(dev)
+
+    def release_model(self) -> None:
+        """Drop the engine's reference to the model (its row-major weights):
+        decode needs only the packed copies; a later prefill() raises."""
+        if self.dense != "packed":
+            raise ValueError("release_model needs dense='packed' (the other paths "
+                             "read the row-major weights every step)")
+        self.model = None
+
+    def hbm_footprint(self) -> dict:
+        """Bytes this engine holds in HBM, by object (torch allocations)."""
+        def nb(t):
+            return t.numel() * t.element_size() if isinstance(t, torch.Tensor) else 0
+        w = 0
+        for lst in (self.wfused, self.wqkv, self.wo, self.ffn_in, self.ffn_out):
+            for W in lst:
+                if W is not None and not W.is_view:
+                    w += W.nbytes()
+        out = {"weights": w,
+               "partial_keys": nb(self.pk),
+               "pool_metadata": nb(self.arrival) + nb(self.lastf) + nb(self.counter),
+               "resident_slots": (nb(getattr(self, "stage_res", None)) +
+                                  nb(getattr(self, "slot_id", None))),
+               "layer0_stage": sum(nb(t) for t in self.stage_full) + sum(nb(t) for t in self.stage_sel),
+               "model_rowmajor": 0}
+        if self.model is not None:
+            seen = set()
+            for lw in self.model.layers:
+                for f in ("w_q", "w_k", "w_v", "w_o", "ffn_in", "ffn_out"):
+                    t = getattr(lw, f)
+                    if isinstance(t, torch.Tensor) and t.is_cuda and t.data_ptr() not in seen:
+                        seen.add(t.data_ptr())
+                        out["model_rowmajor"] += nb(t)
+        out["torch_allocated"] = int(torch.cuda.memory_allocated(self.device))
+        out["host_pool"] = int(self.pool.nbytes) if hasattr(self.pool, "nbytes") else None
+        return out
 
     def _alloc(self) -> None:
         dev, B, L, Hg, d, S, cap = self.device, self.B, self.L, self.Hg, self.d, self.S_max, self.cap
@@ -515,7 +613,6 @@ class DecodeEngine:
             ksp = self._ksplit(B, N_, K_)
             self.gemm_ksplit[(N_, K_)] = ksp
             ws = max(ws, ((N_ + 127) // 128) * ksp * B * 128)
-        self._packed = {}
         if self.dense == "packed":
             ws = 0
             for N_, K_ in shapes:
@@ -523,7 +620,6 @@ class DecodeEngine:
                 _lib.call("ig_sgemm_packed_sizes", min(B, PACKED_MAX_M), N_, K_, None, ctypes.byref(wf),
                           None, kernels=0)
                 ws = max(ws, wf.value)
-            self._pack_weights()
         self.gemm_ws = torch.empty(ws, dtype=f32, device=dev)
         self.gemm_tickets = torch.zeros(max((N_ + 127) // 128 for N_, _ in shapes), dtype=i32, device=dev)
         pf, tk = ctypes.c_size_t(), ctypes.c_size_t()
@@ -726,16 +822,27 @@ class DecodeEngine:
 
     # ---------------------------------------------------------------- prefill
     @torch.no_grad()
-    def prefill(self, prompts, tf32: bool = False) -> None:
+    def prefill(self, prompts, tf32: bool = False, chunk_rows: int = 1 << 16,
+                dense: str = "tc05") -> None:
         """GPU prefill of all B prompts (engine.py:245-291).  prompts: [B, N, D].
 
-        tf32=True runs the prefill GEMMs on TF32 tensor cores (bench setup of
-        the 13B-class shapes); the default keeps IEEE fp32 like the reference.
+        Layer-outer and batched over the sequences: layer li's weights are
+        split once into tcgen05 operands (dense="tc05", the default:
+        csrc/gemm_tc05.cu, f32-level hi/lo split GEMMs with the ReLU and the
+        residual adds fused into their epilogues), every sequence runs through
+        the layer in groups of at most `chunk_rows` prompt rows, and the K/V
+        rows, partial columns and partial keys of layer li are written without a
+        host synchronisation.  dense="torch": cuBLAS GEMMs instead, IEEE fp32, or
+        TF32 with tf32=True (A/B only).
         """
         self._need_group()
+        if dense not in ("tc05", "torch"):
+            raise ValueError("dense must be 'tc05' or 'torch'")
+        from . import tcgemm
         cfg, spec = self.config, self.spec
         L, B, Hg, d, S, D = self.L, self.B, self.Hg, self.d, self.S_max, self.D
         N = cfg.prompt_len
+        Hgd = Hg * d
         prompts = _f32(prompts, self.device).reshape(B, N, D)
         row_of, arr, lf, ct, ovw = _simulate_prefill_rows(N, cfg.pool_limit, self.policy)
         keep_tok = np.full(len(arr), -1, np.int64)
@@ -744,40 +851,91 @@ class DecodeEngine:
         rows = len(arr)
         keep = torch.from_numpy(keep_tok).to(self.device)
         T = _TORCH_ELT[self.elt]
+        spec_ = self.scheme == "speculative"
+        seqs = max(1, min(B, chunk_rows // max(N, 1)))       # sequences per group
+        x_all = prompts.reshape(B * N, D).clone()
+        del prompts
+        tc = dense == "tc05"
+        ws = {}                                   # split-operand buffers, reused per layer
+
+        def mm(X, Wop, Wrm, key, epilogue=0, R=None):
+            if tc:
+                A = tcgemm.split_rows(X, ws.get(key))
+                ws[key] = A
+                return tcgemm.gemm(A, Wop, M=X.shape[0], epilogue=epilogue, R=R)
+            y = X @ Wrm
+            if epilogue == 1:
+                y.relu_()
+            elif epilogue == 2:
+                y += R
+            return y
+
         old = torch.backends.cuda.matmul.allow_tf32
         torch.backends.cuda.matmul.allow_tf32 = bool(tf32)
         try:
-            for b in range(B):
-                x = prompts[b]
-                for li in range(L):
-                    g1, b1, g2, b2 = self.ln[li]
+            for li in range(L):
+                g1, b1, g2, b2 = self.ln[li]
+                W = (self._layer_rowmajor(li) if self.dense == "packed" else
+                     {"qkvq": (self.wfused[li] or self.wqkv[li]).rm, "wo": self.wo[li].rm,
+                      "ffn_in": self.ffn_in[li].rm, "ffn_out": self.ffn_out[li].rm})
+                wqkv = W["qkvq"][:, :3 * Hgd]
+                if tc:
+                    ops = {"qkv": tcgemm.split_weight(wqkv.contiguous()),
+                           "wo": tcgemm.split_weight(W["wo"]),
+                           "ffn_in": tcgemm.split_weight(W["ffn_in"]),
+                           "ffn_out": tcgemm.split_weight(W["ffn_out"])}
+                    del W, wqkv
+                    W, wqkv = None, None
+                else:
+                    ops = {"qkv": None, "wo": None, "ffn_in": None, "ffn_out": None}
+                    W = dict(W, qkv=wqkv)
+                rm = W or {"qkv": None, "wo": None, "ffn_in": None, "ffn_out": None}
+                for b0 in range(0, B, seqs):
+                    nb = min(seqs, B - b0)
+                    x = x_all[b0 * N:(b0 + nb) * N]
                     x_a = layernorm(x, g1, b1, spec.ln_eps)
-                    qkv = x_a @ self.wqkv[li]
-                    q, k, v = (qkv[:, i * Hg * d:(i + 1) * Hg * d].reshape(N, Hg, d).transpose(0, 1)
-                               for i in range(3))
-                    att = causal_attention(q.contiguous(), k.contiguous(), v.contiguous())
-                    o = att.transpose(0, 1).reshape(N, Hg * d) @ self.wo[li]
+                    qkv = mm(x_a, ops["qkv"], rm["qkv"], "x").view(nb, N, 3, Hg, d)
+                    del x_a
+                    att = torch.empty((nb, N, Hg, d), dtype=torch.float32, device=self.device)
+                    for j in range(nb):
+                        q, k, v = (qkv[j, :, i].transpose(0, 1).contiguous() for i in range(3))
+                        att[j] = causal_attention(q, k, v).transpose(0, 1)
+                        b = b0 + j
+                        # pool rows (keep_tok: which prompt token survives in each row)
+                        kvrows = torch.stack([k[:, keep], v[:, keep]], dim=2).to(T).contiguous()
+                        base = self._pool_layer_host(li) + b * Hg * S * self.row_bytes
+                        _lib.call("ig_memcpy2d", base, S * self.row_bytes, kvrows.data_ptr(),
+                                  rows * self.row_bytes, rows * self.row_bytes, Hg,
+                                  _lib.stream_handle(), kernels=0)
+                        if li >= 1 and spec_:
+                            cols = partial_columns(q, k, cfg.speculation.partial_ratio)
+                            self.cols[li, b] = cols
+                            ksel = torch.gather(k[:, keep], 2,
+                                                cols.long()[:, None, :].expand(Hg, rows, self.kcols))
+                            self.pk[li - 1, b, :, :, :rows] = ksel.transpose(1, 2)
+                        del q, k, v, kvrows
+                    del qkv
                     if self.world > 1:
+                        o = mm(att.view(nb * N, Hgd), ops["wo"], rm["wo"], "att")
                         dist.all_reduce(o, group=self.group)
-                    mid = x + o
+                        mid = o.add_(x)
+                    else:                              # x_mid = x + attn @ W_O, fused
+                        mid = mm(att.view(nb * N, Hgd), ops["wo"], rm["wo"], "att", 2, x)
+                    del att
                     xf = layernorm(mid, g2, b2, spec.ln_eps)
-                    ffn = torch.relu(xf @ self.ffn_in[li]) @ self.ffn_out[li]
+                    hid = mm(xf, ops["ffn_in"], rm["ffn_in"], "x", 1)
+                    del xf
                     if self.Fg != self.F:
+                        ffn = mm(hid, ops["ffn_out"], rm["ffn_out"], "hid")
                         dist.all_reduce(ffn, group=self.group)   # row-parallel FFN-out
-                    x = mid + ffn
-                    # pool rows (keep_tok: which prompt token survives in each row)
-                    kvrows = torch.stack([k[:, keep], v[:, keep]], dim=2).to(T).contiguous()
-                    base = self._pool_layer_host(li) + b * Hg * S * self.row_bytes
-                    _lib.call("ig_memcpy2d", base, S * self.row_bytes, kvrows.data_ptr(),
-                              rows * self.row_bytes, rows * self.row_bytes, Hg,
-                              _lib.stream_handle(), kernels=0)
-                    if li >= 1 and self.scheme == "speculative":
-                        cols = partial_columns(q, k, cfg.speculation.partial_ratio)
-                        self.cols[li, b] = cols
-                        ksel = torch.gather(k[:, keep], 2, cols.long()[:, None, :].expand(Hg, rows, self.kcols))
-                        self.pk[li - 1, b, :, :, :rows] = ksel.transpose(1, 2)
-                    torch.cuda.current_stream().synchronize()  # kvrows lifetime
-                self.x[b] = x[-1]
+                        x.copy_(mid.add_(ffn))
+                        del ffn
+                    else:                              # x = x_mid + FFN, fused
+                        x.copy_(mm(hid, ops["ffn_out"], rm["ffn_out"], "hid", 2, mid))
+                    del hid, mid
+                del ops, W, rm
+            self.x.copy_(x_all.view(B, N, D)[:, -1])
+            del x_all, ws
         finally:
             torch.backends.cuda.matmul.allow_tf32 = old
         self.arrival[..., :rows] = torch.from_numpy(arr).to(self.device)
@@ -1006,39 +1164,17 @@ class DecodeEngine:
         lib = _lib.load()
         return lib.ig_sgemm_tc_ksplit(M, N, K) if self.dense == "tc" else lib.ig_sgemm_rows_ksplit(M, N, K)
 
-    def _pack_weights(self) -> None:
-        """dense="packed": re-lay every decode-step weight once into the
-        ig_sgemm_packed block format (same bytes as f32).  The row-major copies
-        stay for the prefill."""
-        spec_ = self.scheme == "speculative"
-        mats = []
-        for li in range(self.L):
-            fused = spec_ and li + 1 < self.L and self.wfused[li] is not None
-            mats += [self.wfused[li] if fused else self.wqkv[li], self.wo[li], self.ffn_in[li],
-                     self.ffn_out[li]]
-        for W in mats:
-            self._packed_weight(W)
-        torch.cuda.synchronize(self.device)
-
-    def _packed_weight(self, W):
-        key = (W.data_ptr(), W.shape[0], W.shape[1], W.stride(0))
-        P = self._packed.get(key)
-        if P is None:
-            K, N = W.shape
-            pf = ctypes.c_size_t()
-            _lib.call("ig_sgemm_packed_sizes", 1, N, K, ctypes.byref(pf), None, None, kernels=0)
-            P = torch.empty(pf.value, dtype=torch.float32, device=self.device)
-            _lib.call("ig_sgemm_pack", W.data_ptr(), W.stride(0), N, K, P.data_ptr(),
-                      torch.cuda.current_stream(self.device).cuda_stream, kernels=2)
-            self._packed[key] = P
-        return P
+    def _packed_weight(self, W: "_Weight"):
+        return W.packed
 
     def _gemm(self, X, W, Y, cs, epilogue: int = 0, R=None) -> None:
         """Y = X @ W (+ ReLU / + R) on the compute stream."""
         M, K = X.shape
-        N = W.shape[1]
+        N = W.N
         if self.dense == "packed":
-            P = self._packed_weight(W)
+            P = W.packed
+            if P is None:
+                raise RuntimeError("packed weights of this matrix are not built")
             if self._inst is not None:
                 self._mark("dense", -1, self.compute, True, 4 * (K * N + M * K + M * N))
             # the packed kernel takes <= 32 rows (its x fragments); larger batches
@@ -1054,7 +1190,7 @@ class DecodeEngine:
                 self._mark("dense", -1, self.compute, False)
             return
         if self.dense == "cublas":
-            res = torch.addmm(R, X, W) if epilogue == 2 else torch.matmul(X, W)
+            res = torch.addmm(R, X, W.rm) if epilogue == 2 else torch.matmul(X, W.rm)
             if epilogue == 1:
                 res.relu_()
             Y.copy_(res)              # Y may be a strided view (qkv of the fused buffer)
@@ -1062,7 +1198,7 @@ class DecodeEngine:
         ksp = self.gemm_ksplit.get((N, K)) or self._ksplit(M, N, K)
         if self._inst is not None:
             self._mark("dense", -1, self.compute, True, 4 * (K * N + M * K + M * N))
-        _lib.call("ig_sgemm_tc" if self.dense == "tc" else "ig_sgemm_rows", X.data_ptr(), X.stride(0), W.data_ptr(), W.stride(0),
+        _lib.call("ig_sgemm_tc" if self.dense == "tc" else "ig_sgemm_rows", X.data_ptr(), X.stride(0), W.rm.data_ptr(), W.rm.stride(0),
                   Y.data_ptr(), Y.stride(0), _lib.ptr(R), R.stride(0) if R is not None else 0,
                   M, N, K, ksp, epilogue, self.gemm_ws.data_ptr(), self.gemm_ws.numel(),
                   self.gemm_tickets.data_ptr(), cs)
@@ -1207,11 +1343,42 @@ class DecodeEngine:
                     C.wait_event(self.ev_sel[li])
                 if li >= 1 and AP is not C:
                     C.wait_event(self.ev_app[li - 1])   # append(li-1) read qkv: free it
+                sel = speculative and li >= 1
+                ldq = self.qkvq.stride(0)
+
+                def do_append(li=li, sel=sel, ldq=ldq):
+                    if AP is not C:
+                        self.ev_qkv[li].record(C)
+                        AP.wait_event(self.ev_qkv[li])
+                    _lib.call("ig_append", self.qkv.data_ptr() + 4 * Hgd, self.qkv.data_ptr() + 8 * Hgd,
+                              ldq, self._pool_layer_dev(li), _lib.ELT[self.elt],
+                              _lib.ptr(self.pk[li - 1]) if sel else None,
+                              _lib.ptr(self.cols[li]) if sel else None, self.kcols,
+                              self.arrival[li].data_ptr(), self.lastf[li].data_ptr(),
+                              self.counter[li].data_ptr(), _lib.POLICY[self.policy.value],
+                              2 if sel else 1, _lib.ptr(self.idx[li]) if sel else None,
+                              _lib.ptr(self.n[li]) if sel else None, self.cap,
+                              self.st.data_ptr(), B, Hg, d, self.S_max, self.pos[li].data_ptr(),
+                              self.events[li].data_ptr(), aps)
+                    if resident and li == 0:            # keep layer 0's mirror complete
+                        _lib.call("ig_stage_put", self.qkv.data_ptr() + 4 * Hgd,
+                                  self.qkv.data_ptr() + 8 * Hgd, ldq, self.pos[0].data_ptr(),
+                                  self.stage_full[0].data_ptr(), _lib.ELT[self.elt], B, Hg, d,
+                                  self.S_max, aps)
+                    if AP is not C:
+                        self.ev_app[li].record(AP)
+                appended = False
                 nxt = li + 1
                 if nxt < L:
                     if speculative:
                         # q/k/v of this layer + the speculation query of the next
                         self._gemm(self.x_a, self.wfused[li], self.qkvq, cs)
+                        if self.append_first and SP is not C:
+                            # the append before the rehearsal is released: both become
+                            # ready together and the high-priority rehearsal would take
+                            # every SM slot first (measured 49 us of append delay at C3)
+                            do_append()
+                            appended = True
                         if SP is not C:
                             self.ev_q[li].record(C)
                             SP.wait_event(self.ev_q[li])
@@ -1281,28 +1448,8 @@ class DecodeEngine:
                     self.ev_fetch[nxt].record(Fs)
                 if not (speculative and nxt < L):      # else computed by the fused GEMM
                     self._gemm(self.x_a, self.wqkv[li], self.qkv, cs)
-                sel = speculative and li >= 1
-                ldq = self.qkvq.stride(0)
-                if AP is not C:
-                    self.ev_qkv[li].record(C)
-                    AP.wait_event(self.ev_qkv[li])
-                _lib.call("ig_append", self.qkv.data_ptr() + 4 * Hgd, self.qkv.data_ptr() + 8 * Hgd,
-                          ldq, self._pool_layer_dev(li), _lib.ELT[self.elt],
-                          _lib.ptr(self.pk[li - 1]) if sel else None,
-                          _lib.ptr(self.cols[li]) if sel else None, self.kcols,
-                          self.arrival[li].data_ptr(), self.lastf[li].data_ptr(),
-                          self.counter[li].data_ptr(), _lib.POLICY[self.policy.value],
-                          2 if sel else 1, _lib.ptr(self.idx[li]) if sel else None,
-                          _lib.ptr(self.n[li]) if sel else None, self.cap,
-                          self.st.data_ptr(), B, Hg, d, self.S_max, self.pos[li].data_ptr(),
-                          self.events[li].data_ptr(), aps)
-                if resident and li == 0:            # keep layer 0's mirror complete
-                    _lib.call("ig_stage_put", self.qkv.data_ptr() + 4 * Hgd,
-                              self.qkv.data_ptr() + 8 * Hgd, ldq, self.pos[0].data_ptr(),
-                              self.stage_full[0].data_ptr(), _lib.ELT[self.elt], B, Hg, d,
-                              self.S_max, aps)
-                if AP is not C:
-                    self.ev_app[li].record(AP)
+                if not appended:
+                    do_append()
                 apos = None if AP is not C else self.pos[li]   # NULL: pos = st.s_len
                 C.wait_event(self.ev_fetch[li])
                 self._mark("attend", li, C, True)

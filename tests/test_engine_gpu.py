@@ -527,6 +527,36 @@ def test_c1_hook_mode_exact():
 
 
 @pytest.mark.slow
+@pytest.mark.slow
+def test_c1_gpu_prefill_matches_oracle():
+    """VERDICT r1 #7 at BASELINE.json configs[0]: the GPU prefill (tcgen05
+    split-precision GEMMs, batched layer-outer) from the reference's own
+    random_prompt vs the oracle's prefill (the reference's CPU path): every
+    pool row within 1e-4, every (layer, head) partial-column choice identical,
+    the last-token state within 1e-4 scaled."""
+    from paper_2406_19707_b200 import DecodeEngine
+    model, ocfg, sessions = _c1_state()
+    eng = DecodeEngine(model, engine_cfg(ocfg), pool_dtype="f32")
+    try:
+        prompts = np.stack([O.random_prompt(ocfg.prompt_len, 768, ocfg.prompt_seed + b)
+                            for b in range(ocfg.batch)])
+        eng.prefill(prompts)
+        pv = eng.pool_view()
+        worst = 0.0
+        for li in range(12):
+            for h in range(12):
+                p = sessions[0].pools[li][h]
+                for got, ref in ((pv[li, 0, h, :len(p), 0], p.keys), (pv[li, 0, h, :len(p), 1], p.values)):
+                    worst = max(worst, float(np.max(np.abs(got - ref) / np.maximum(1.0, np.abs(ref)))))
+                if li >= 1:
+                    np.testing.assert_array_equal(eng.cols[li, 0, h].cpu().numpy(),
+                                                  sessions[0].artifacts.head(li, h).column_indices)
+        assert worst < 1e-4, worst
+        assert _scaled_err(eng.x.cpu().numpy(), sessions[0].x[None]) < 1e-4
+    finally:
+        eng.close()
+
+
 def test_c1_opt125m_shape_end_to_end():
     """BASELINE.json configs[0]: OPT-125M shape (12 x 768, 12 heads, d 64),
     2048-token prompt, alpha 4, ratio 0.3.  The oracle skews and prefills (the

@@ -56,8 +56,10 @@ def main():
     g = torch.Generator(device=dev)
     g.manual_seed(1234)
     prompts = torch.empty(a.batch, a.prompt, spec.model_dim, device=dev).normal_(generator=g)
-    eng.prefill(prompts, tf32=True)
+    eng.prefill(prompts)
     del prompts
+    eng.release_model()
+    torch.cuda.empty_cache()
     for _ in range(4):
         eng.decode_step()
     torch.cuda.synchronize()
