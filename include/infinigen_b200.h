@@ -314,6 +314,12 @@ int ig_gemm_tc05(const void* A_hl, const float* inv_sa, const void* B_hl, const 
                  int N, int K, int Kp, float* C, int ldc, const float* R, int ldr, int epilogue,
                  int max_ctas, void* stream);
 
+/* ---- diagnostics --------------------------------------------------------
+ * ig_debug_attend_trace: device buffer (u64, >= grid x (8 + 6 x 64)) that the
+ * tcgen05 attention fills with %globaltimer stamps per role and tile
+ * (tools/attend_trace.py); NULL switches it off (the default). */
+int ig_debug_attend_trace(void* buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,6 +8,7 @@
 // result is deterministic.  Scores are (q . k) / float32(sqrt(d)) -- a division,
 // as in model.py:174 -- and exp is the full-precision expf.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -1214,13 +1215,19 @@ attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restric
 // (round 1): register-fed 2.84 TB/s vs TMA-fed 2.39 TB/s -- the per-row math
 // (f16 unpack + shuffle reductions), not the feed, bounds this kernel, so
 // the register-fed loop stays the default.
-inline char attend_impl() {   // 'm' (default, tensor cores), 'r' (register-fed), 't' (TMA-fed)
+// 'c' (default: tcgen05, attend_tc05.cu), 'm' (mma.sync), 'r' (register-fed), 't' (TMA-fed)
+inline char attend_impl() {
   static const char impl = [] {
     const char* v = getenv("IG_ATTEND_IMPL");
-    return v && (v[0] == 'r' || v[0] == 't') ? v[0] : 'm';
+    return v && (v[0] == 'r' || v[0] == 't' || v[0] == 'm') ? v[0] : 'c';
   }();
   return impl;
 }
+
+int attend_tc05_launch(int elt, cudaStream_t s, const float* q, int ldq, const float* k_cur, const float* v_cur,
+                       int ldkv, const void* stage, const int32_t* idx, const int32_t* n, const int32_t* rows_bh,
+                       const int32_t* pos, const ig_step_state* st, int B, int Hg, int cap, float sqrt_d,
+                       int max_chunks, float* partial, int32_t* tickets, float* out, int ldo);
 inline bool attend_tma_enabled() { return attend_impl() == 't'; }
 
 template <typename T>
@@ -1230,6 +1237,21 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
                   const ig_step_state* st, int Hg, int d, int cap, float sqrt_d, int max_chunks,
                   float* partial, int32_t* tickets, float* out, int ldo) {
   if constexpr (sizeof(T) == 2) {
+    // tcgen05 (attend_tc05.cu) for row sets above 2K rows (layer 0's full
+    // mirror, long-context selections: 6.07 vs 5.94 TB/s at 4K rows), the
+    // mma.sync warp-persistent kernel below (68 vs 73 us at C3's 819 rows,
+    // tools/attend_trace.py); IG_ATTEND_IMPL=c forces tcgen05 everywhere.
+    // -1 from the launcher: not applicable here.
+    static const bool force_c = [] {
+      const char* v = getenv("IG_ATTEND_IMPL");
+      return v && v[0] == 'c';
+    }();
+    if (d == 128 && attend_impl() == 'c' && (cap > 2048 || force_c)) {
+      const int rc = attend_tc05_launch(std::is_same<T, __half>::value ? IG_ELT_F16 : IG_ELT_BF16, s, q, ldq, k_cur,
+                                        v_cur, ldkv, stage, idx, n, rows_bh, pos, st, (int)grid.z, Hg, cap, sqrt_d,
+                                        max_chunks, partial, tickets, out, ldo);
+      if (rc >= 0) return rc;
+    }
     if (d == 128 && attend_tma_enabled()) {  // 512-B rows, TMA-fed (opt-in)
       const int mc = (cap + kTmaChunk - 1) / kTmaChunk;
       const size_t smem = (size_t)kTmaStages * kTmaRows * 512;
@@ -1241,7 +1263,7 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
       IG_LAUNCH_STATUS();
       return IG_OK;
     }
-    if (d == 128 && attend_impl() == 'm') {  // 512-B rows on the tensor cores (default)
+    if (d == 128 && (attend_impl() == 'm' || attend_impl() == 'c')) {  // 512-B rows, mma.sync
       // IG_ATT_VARIANT (tuning sweeps): 0 = CTA per chunk, ring 2 x 8 tiles/warp (3 CTAs/SM),
       // 1 = ring 2 x 4 tiles, 2 = ring 3 x 8 tiles (2 CTAs/SM), 3 = ring 2 x 16 tiles,
       // 4 = warp-persistent (attend512_wp_kernel)
