@@ -463,15 +463,22 @@ inline int grid_for(int N, int K, int cps) {
   return (int)G;
 }
 
+// IG_PACKED_CTA: 0 (default) 2 x 8-warp CTAs per SM; 16: one 16-warp CTA, 6-deep
+// ring; 8: one 8-warp CTA, 3-deep ring (half the SM's registers and shared
+// memory left to the kernels of the other streams)
+inline int packed_cta_mode() {
+  static const int m = [] {
+    const char* e = getenv("IG_PACKED_CTA");
+    return e ? atoi(e) : 0;
+  }();
+  return m == 16 || m == 8 ? m : 0;
+}
+
 inline int ctas_per_sm(int M) {
   // IG_PACKED_CTA=16: one 16-warp CTA per SM with a 6-deep ring (more bytes in
   // flight, fewer CTA fix-ups) -- measured equal or slower (ffn_out 4.7 vs 5.6
   // TB/s), so 2 x 8-warp CTAs stay the default
-  static const int wide = [] {
-    const char* e = getenv("IG_PACKED_CTA");
-    return e && atoi(e) == 16 ? 1 : 0;
-  }();
-  return M <= 16 && !wide ? 2 : 1;
+  return M <= 16 && packed_cta_mode() == 0 ? 2 : 1;
 }
 
 template <int NB, int CPS, int STAGES, int KG>
@@ -544,6 +551,10 @@ static int sgemm_packed_any(const float* X, int ldx, const float* P, int N, int 
   ig_sgemm_packed_sizes(M, N, K, nullptr, &ws_need, &tk_need);
   if (ws_need > workspace_floats || tk_need > ntickets) return IG_EINVAL;
   if (M > 16) return launch<4, 1, 6, 2>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s, po);
+  if (ctas_per_sm(M) == 1 && packed_cta_mode() == 8) {      // 8 warps, 3-deep ring, 1 CTA/SM
+    if (M <= 8) return launch<1, 1, 3, 2>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s, po);
+    return launch<2, 1, 3, 2>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s, po);
+  }
   if (ctas_per_sm(M) == 1) {      // 16 warps, 6-deep ring
     if (M <= 8) return launch<1, 1, 6, 4>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s, po);
     return launch<2, 1, 6, 4>(X, ldx, P, Y, ldy, R, ldr, M, N, K, epilogue, workspace, tickets, s, po);
