@@ -73,7 +73,8 @@ def _args():
     ap.add_argument("--no-variant", "--no-hbm-variant", dest="no_variant", action="store_true",
                     help="skip the secondary run (resident: refetch every step; else layer 0 in HBM)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-steps", type=int, default=2)
+    ap.add_argument("--cpu-sample-steps", type=int, default=None,
+                    help="timed 3-layer steps of the CPU baseline (default: --steps, as the reference arm)")
     return ap.parse_args()
 
 
@@ -183,7 +184,12 @@ def cpu_reference(shape: str, batch: int, prompt: int, steps: int, warmup: int =
                        f"{shape} truncation, s={prompt}, 1 sequence, {len(per_layer)} timed steps; "
                        f"T_step = T0 + {L_full - 2}*T1 + T_last = {t_seq:.3f} s/seq, batch {batch} "
                        f"runs serially -> {batch} tok per {batch * t_seq:.2f} s (extrapolated)"),
-            "t_layer0_s": t0_, "t_layer_mid_s": t1_, "t_layer_last_s": tl_, "t_seq_s": t_seq}
+            "t_layer0_s": t0_, "t_layer_mid_s": t1_, "t_layer_last_s": tl_, "t_seq_s": t_seq,
+            "measured": {"what": f"median {Lt}-layer truncation decode_step, 1 sequence (wall clock)",
+                         "step_s": t0_ + t1_ + tl_, "timed_steps": len(per_layer)},
+            "extrapolated": {"what": f"{L_full} layers x batch {batch} (run() serialises the batch, "
+                                     "engine.py:468-476)",
+                             "step_s": batch * t_seq}}
 
 
 def run_reference_arm(a) -> None:
@@ -385,8 +391,24 @@ def run_b200(a) -> None:
         eng._inst = None
         eng.set_hbm_layers(0)
     ms_t = torch.tensor([ms, e2e_ms, var_ms], dtype=torch.float64, device=dev)
+    # per rank (N > 1: the scaling curve's evidence): its own step time, the
+    # kernels on its GPU, what its fetch stream moved over its host link, and
+    # where its host pool lives
+    mine = {"rank": rank, "ms_per_step": ms / a.steps, "heads": eng.Hg,
+            "host_pool_numa_node": eng.pool.numa_node,
+            "kernels_ms_per_step": {k: v["ms"] / a.steps for k, v in stats.items()
+                                    if isinstance(v, dict) and v.get("ms")},
+            "hbm_footprint_gb": footprint["torch_allocated"] / 1e9}
+    fk = [v for k, v in stats.items() if isinstance(v, dict) and k.startswith("fetch") and v.get("ms")]
+    if fk:
+        fb, fm = sum(v["bytes"] for v in fk), sum(v["ms"] for v in fk)
+        mine["fetch_link_gbs"] = fb / (fm * 1e6) if fm else None
+        mine["fetch_bytes_per_step"] = fb / a.steps
+    per_rank = [mine]
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
     ms, e2e_ms, var_ms = float(ms_t[0]), float(ms_t[1]), float(ms_t[2])
 
     if rank == 0:
@@ -451,6 +473,7 @@ def run_b200(a) -> None:
                         "h2d_bytes_per_step": a.batch * spec.model_dim * 4,
                         "d2h_bytes_per_step": a.batch * spec.model_dim * 4},
                 "gpu_launches": launches, "setup_s": setup_s, "prefill_s": prefill_s,
+                "per_rank": per_rank,
                 "hbm_footprint_gb": {k: (v / 1e9 if isinstance(v, int) else v)
                                      for k, v in footprint.items()},
                 "link_bytes_per_step": {"reference_accounted": _ref_bytes(stats, eng, a.steps),
@@ -474,7 +497,8 @@ def run_b200(a) -> None:
                 "kernel_stats": var_stats}
         if not a.no_cpu_baseline and world == 1:
             try:
-                line["cpu_baseline"] = cpu_reference(a.shape, a.batch, a.prompt, a.cpu_sample_steps)
+                line["cpu_baseline"] = cpu_reference(a.shape, a.batch, a.prompt,
+                                                     a.cpu_sample_steps or a.steps)
             except Exception as e:  # reported, never fatal to the GPU number
                 line["cpu_baseline"] = {"error": repr(e)}
         print(json.dumps(line), flush=True)

@@ -64,6 +64,10 @@ const char* ig_status_string(int status);
 /* Pinned, mapped, portable host allocation; *dev_ptr is its device alias.   */
 int ig_host_alloc(size_t bytes, void** host_ptr, void** dev_ptr);
 int ig_host_free(void* host_ptr);
+/* NUMA node holding the pool's first page (-1: unknown).  ig_host_alloc binds
+ * the pool to the current GPU's NUMA node when the machine has several nodes
+ * (mmap + mbind + cudaHostRegister; IG_HOST_NUMA=0: plain cudaHostAlloc). */
+int ig_host_numa_node(const void* host_ptr, int* node);
 
 /* ---- K1 rehearsal: replaces speculate_scores (speculation.py:117-135) -----
  * qspec = x_a(prev layer) @ W_Q(layer)[:, local heads] (f32[B][ldq]).  Per

@@ -31,6 +31,7 @@ _SIGS = {
     "ig_abi_version": [],
     "ig_host_alloc": [_SZ, ctypes.POINTER(_P), ctypes.POINTER(_P)],
     "ig_host_free": [_P],
+    "ig_host_numa_node": [_P, ctypes.POINTER(_I)],
     "ig_rehearse": [_P, _I, _P, _P, _P, _I, _I, _I, _I, _I, _F, _P, _P, _P],
     "ig_rehearse_count": [_P, _I, _P, _P, _P, _I, _I, _I, _I, _I, _F, _D, _P, _P, _P, _P, _P, _P],
     "ig_count": [_P, _P, _P, _I, _I, _I, _D, _P, _P, _P],

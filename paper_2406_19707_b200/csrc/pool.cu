@@ -387,16 +387,80 @@ __global__ void step_advance_kernel(ig_step_state* st) {
 
 }  // namespace ig
 
+// ---------------------------------------------------------------------------
+// Host pool allocation (each rank's slice of the pinned pool
+// sits on its GPU's NUMA node).  When the machine has more than one NUMA node
+// and the current GPU reports one (sysfs numa_node of its PCI function), the
+// pool is mmap'ed, bound to that node (mbind MPOL_BIND) and pinned + mapped
+// with cudaHostRegister; otherwise (one node, unknown node, IG_HOST_NUMA=0 or
+// any failure) it is a plain cudaHostAlloc(Mapped | Portable).
+// ---------------------------------------------------------------------------
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <cstdio>
+#include <mutex>
+#include <unordered_map>
+
+namespace ig {
+namespace hostpool {
+std::mutex mu;
+std::unordered_map<void*, size_t> mapped;    // mmap'ed + registered pools -> bytes
+
+int gpu_numa_node() {
+  const char* e = getenv("IG_HOST_NUMA");
+  if (e && atoi(e) == 0) return -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof(bus), dev) != cudaSuccess) return -1;
+  for (char* c = bus; *c; ++c) *c = (char)tolower(*c);
+  char path[128];
+  snprintf(path, sizeof(path), "/sys/bus/pci/devices/%s/numa_node", bus);
+  FILE* f = fopen(path, "r");
+  if (!f) return -1;
+  int node = -1;
+  if (fscanf(f, "%d", &node) != 1) node = -1;
+  fclose(f);
+  if (node < 0 || node > 63) return -1;
+  if (access("/sys/devices/system/node/node1", F_OK) != 0) return -1;   // a single node
+  return node;
+}
+}  // namespace hostpool
+}  // namespace ig
+
+extern "C" int ig_host_free(void* host_ptr);
+
 extern "C" int ig_host_alloc(size_t bytes, void** host_ptr, void** dev_ptr) {
+  using namespace ig::hostpool;
   if (!host_ptr || !dev_ptr || bytes == 0) return IG_EINVAL;
   void* h = nullptr;
-  cudaError_t e = cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
-  if (e == cudaErrorMemoryAllocation) return IG_ENOMEM;
-  IG_CUDA_STATUS(e);
+  const int node = gpu_numa_node();
+  if (node >= 0) {
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p != MAP_FAILED) {
+      unsigned long mask = 1ul << node;
+      const long rc = syscall(SYS_mbind, p, bytes, 2 /*MPOL_BIND*/, &mask, 65ul, 0u);
+      if (rc == 0 && cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable) == cudaSuccess) {
+        h = p;
+        std::lock_guard<std::mutex> g(mu);
+        mapped[p] = bytes;
+      } else {
+        cudaGetLastError();
+        munmap(p, bytes);
+      }
+    }
+  }
+  if (!h) {
+    cudaError_t e = cudaHostAlloc(&h, bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e == cudaErrorMemoryAllocation) return IG_ENOMEM;
+    IG_CUDA_STATUS(e);
+  }
   void* d = nullptr;
-  e = cudaHostGetDevicePointer(&d, h, 0);
+  cudaError_t e = cudaHostGetDevicePointer(&d, h, 0);
   if (e != cudaSuccess) {
-    cudaFreeHost(h);
+    ig_host_free(h);
     return IG_ECUDA + (int)e;
   }
   *host_ptr = h;
@@ -405,8 +469,32 @@ extern "C" int ig_host_alloc(size_t bytes, void** host_ptr, void** dev_ptr) {
 }
 
 extern "C" int ig_host_free(void* host_ptr) {
+  using namespace ig::hostpool;
   if (!host_ptr) return IG_EINVAL;
+  size_t bytes = 0;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = mapped.find(host_ptr);
+    if (it != mapped.end()) {
+      bytes = it->second;
+      mapped.erase(it);
+    }
+  }
+  if (bytes) {
+    IG_CUDA_STATUS(cudaHostUnregister(host_ptr));
+    munmap(host_ptr, bytes);
+    return IG_OK;
+  }
   IG_CUDA_STATUS(cudaFreeHost(host_ptr));
+  return IG_OK;
+}
+
+extern "C" int ig_host_numa_node(const void* host_ptr, int* node) {
+  // NUMA node of the pool's first page (get_mempolicy MPOL_F_NODE | MPOL_F_ADDR), -1 if unknown
+  if (!host_ptr || !node) return IG_EINVAL;
+  int n = -1;
+  const long rc = syscall(SYS_get_mempolicy, &n, nullptr, 0ul, const_cast<void*>(host_ptr), 3u);
+  *node = rc == 0 ? n : -1;
   return IG_OK;
 }
 

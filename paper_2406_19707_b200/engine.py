@@ -123,12 +123,16 @@ class _Weight:
 
 
 class HostPool:
-    """Pinned, mapped, portable host memory for the KV rows (ig_host_alloc)."""
+    """Pinned, mapped, portable host memory for the KV rows (ig_host_alloc: on
+    the current GPU's NUMA node when the machine has several)."""
 
     def __init__(self, nbytes: int):
         host, dev = ctypes.c_void_p(), ctypes.c_void_p()
         _lib.call("ig_host_alloc", nbytes, ctypes.byref(host), ctypes.byref(dev), kernels=0)
         self.host, self.dev, self.nbytes = host.value, dev.value, nbytes
+        node = ctypes.c_int(-1)
+        _lib.call("ig_host_numa_node", self.host, ctypes.byref(node), kernels=0)
+        self.numa_node = node.value
 
     def numpy(self, dtype, shape) -> np.ndarray:
         """Host view (no copy) -- inspection and tests."""

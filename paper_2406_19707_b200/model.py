@@ -145,11 +145,14 @@ def generate_synthetic_gpu(spec: ModelSpec, device="cuda", seed: int | None = No
 
 
 def skew_model_gpu(model: Model, calib_tokens: int | None = None, seed: int = 0,
-                   calib_input=None) -> Model:
+                   calib_input=None, forward_dtype=None) -> Model:
     """Offline skew (skewing.py:30-104) on the GPU, in place: forward a
     seeded 4*d-row calibration prompt, SVD each head's Q (f64), take A = V with
     the max-|entry|-positive sign rule (skewing.py:59-66), fold A into the
-    W_Q / W_K head slices."""
+    W_Q / W_K head slices.  The blocks are kept as model.skew_matrices
+    ([L][H] d x d, f64 numpy) with their singular values (model.skew_sigmas),
+    like the reference's SkewSet (skewing.py:14-27).  forward_dtype=float64
+    runs the calibration forward in f64 (the oracle's q are f32 NumPy)."""
     import torch
     from . import prefill as _pf
     spec = model.spec
@@ -162,18 +165,29 @@ def skew_model_gpu(model: Model, calib_tokens: int | None = None, seed: int = 0,
         g = torch.Generator(device=dev)
         g.manual_seed(seed)
         x = torch.empty(max(n, 2), spec.model_dim, device=dev).normal_(generator=g)
+    mats, sigmas = [], []
     for lw in model.layers:
-        out, q = _pf.dense_block_forward(x, lw, spec)
+        if forward_dtype is not None and forward_dtype != torch.float32:
+            lw64 = type(lw)(**{f: getattr(lw, f).to(forward_dtype) for f in LAYER_FIELDS})
+            out, q = _pf.dense_block_forward(x.to(forward_dtype), lw64, spec)
+            out = out.float()
+        else:
+            out, q = _pf.dense_block_forward(x, lw, spec)
         qh = q.view(q.shape[0], spec.heads, d).permute(1, 0, 2).double()  # H x n x d
-        _, _, vh = torch.linalg.svd(qh, full_matrices=False)
+        _, sv, vh = torch.linalg.svd(qh, full_matrices=False)
         a = vh.transpose(1, 2)                                           # H x d x d (= V)
         piv = a.abs().argmax(dim=1, keepdim=True)
         sign = torch.sign(torch.gather(a, 1, piv))
         sign[sign == 0] = 1
-        a = (a * sign).float()
+        a = a * sign
+        mats.append(a.cpu().numpy())
+        sigmas.append(sv.cpu().numpy())
+        a = a.float()
         for which in ("w_q", "w_k"):
             w = getattr(lw, which).view(spec.model_dim, spec.heads, d)
             w.copy_(torch.einsum("Dhi,hij->Dhj", w, a))
         x = out
     model.skewed = True
+    model.skew_matrices = mats
+    model.skew_sigmas = sigmas
     return model

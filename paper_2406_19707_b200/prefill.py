@@ -22,7 +22,14 @@ from . import _lib
 
 def layernorm(x: torch.Tensor, gain: torch.Tensor, bias: torch.Tensor, eps: float,
               out: torch.Tensor | None = None) -> torch.Tensor:
-    """Reference layernorm (linalg.py:50-69) via ig_layernorm."""
+    """Reference layernorm (linalg.py:50-69) via ig_layernorm; f64 inputs (the
+    offline skew's optional f64 calibration forward) in f64 torch ops."""
+    if x.dtype == torch.float64:
+        mean = x.mean(dim=-1, keepdim=True)
+        c = x - mean
+        var = (c * c).mean(dim=-1, keepdim=True)
+        y = c / torch.sqrt(var + eps) * gain.to(x.dtype) + bias.to(x.dtype)
+        return y if out is None else out.copy_(y)
     x = x.contiguous()
     rows, D = x.shape
     y = torch.empty_like(x) if out is None else out
