@@ -357,7 +357,8 @@ class DecodeEngine:
                  fetch_threads: int = 32, fetch_priority: int = 0, hbm_layers: int = 0,
                  fetch_impl: str = "tma", fetch_rows: int = 16, dense: str = "packed",
                  cuda_graph: bool = False, resident: bool | None = None, spec_stream: bool = True,
-                 append_stream: bool = False, shard: tuple[int, int] | None = None):
+                 append_stream: bool = False, shard: tuple[int, int] | None = None,
+                 record_trace: bool = False):
         config.validate()
         _lib.load()
         _enable_ieee_fp32()
@@ -438,6 +439,10 @@ class DecodeEngine:
         self._res_valid = False
         self.spec_stream_on = bool(spec_stream)
         self.append_stream_on = bool(append_stream)
+        # per-layer LayerRecords (bytes, n, pool events; engine.py:420-437) even
+        # without record_selection / record_scores -- what the reference's run()
+        # always keeps (one host sync per layer: a trace mode, not the perf path)
+        self.record_trace = bool(record_trace)
         # IG_APPEND_FIRST=1: launch ig_append(li) before releasing the speculation
         # chain of li+1 (measured at C3: 952 vs 984 tok/s -- off)
         self.append_first = os.environ.get("IG_APPEND_FIRST", "0") == "1"
@@ -581,9 +586,13 @@ class DecodeEngine:
         self.x_a = torch.empty((B, D), dtype=f32, device=dev)
         self.x_f = torch.empty((B, D), dtype=f32, device=dev)
         # [q | k | v | qspec(next layer)] per sequence, one row of the fused GEMM
-        self.qkvq = torch.empty((B, 4 * Hg * d), dtype=f32, device=dev)
-        self.qkv = self.qkvq[:, :3 * Hg * d]
-        self.qspec = self.qkvq[:, 3 * Hg * d:]
+        # two [q | k | v | qspec] buffers by layer parity (IG_QKV_DB=1; default one): layer
+        # li's GEMM then only waits for the speculation chain of li before its
+        # append, not before the GEMM (which overwrites the other parity's qspec)
+        self.qkv_db = os.environ.get("IG_QKV_DB", "0") == "1"    # measured neutral (987 vs 990)
+        self.qkvq_buf = [torch.empty((B, 4 * Hg * d), dtype=f32, device=dev)
+                         for _ in range(2 if self.qkv_db else 1)]
+        self._use_qkv(0)
         self.attn = torch.empty((B, Hg * d), dtype=f32, device=dev)
         self.o = torch.empty((B, D), dtype=f32, device=dev)
         self.hidden = torch.empty((B, self.Fg), dtype=f32, device=dev)
@@ -643,6 +652,13 @@ class DecodeEngine:
         self.ev_fetch = [torch.cuda.Event() for _ in range(L)]
         self.ev_att = [torch.cuda.Event() for _ in range(L)]
         self.ev_step = torch.cuda.Event()
+
+    def _use_qkv(self, li: int) -> None:
+        """Bind qkvq / qkv / qspec to layer li's buffer."""
+        Hgd = self.Hg * self.d
+        self.qkvq = self.qkvq_buf[li % len(self.qkvq_buf)]
+        self.qkv = self.qkvq[:, :3 * Hgd]
+        self.qspec = self.qkvq[:, 3 * Hgd:]
 
     def _alloc_resident(self) -> None:
         dev, B, L, Hg, d, cap = self.device, self.B, self.L, self.Hg, self.d, self.cap
@@ -1302,7 +1318,7 @@ class DecodeEngine:
         sps = SP.cuda_stream
         s = self.s_host
         graph = self._graph_mode
-        recording = (cfg.record_selection or cfg.record_scores) and not graph
+        recording = (cfg.record_selection or cfg.record_scores or self.record_trace) and not graph
         # append stream: without a pool limit the append position is st.s_len, so the
         # attention does not wait for ig_append, which then runs beside it
         AP = (self.append_stream if (self.append_stream_on and cfg.pool_limit is None and not recording)
@@ -1339,10 +1355,12 @@ class DecodeEngine:
                 self.ev_fetch[0].record(Fs)
             x = self.x
             for li in range(L):
+                self._use_qkv(li)
                 g1, b1, g2, b2 = self.ln[li]
                 _lib.call("ig_layernorm", x.data_ptr(), g1.data_ptr(), b1.data_ptr(),
                           float(spec.ln_eps), B, self.D, self.x_a.data_ptr(), cs)
-                if speculative and li >= 1 and SP is not C:
+                spec_wait = speculative and li >= 1 and SP is not C
+                if spec_wait and not self.qkv_db:
                     # spec(li) done: qspec is free for the fused GEMM, idx/n/plan of li ready
                     C.wait_event(self.ev_sel[li])
                 if li >= 1 and AP is not C:
@@ -1351,6 +1369,10 @@ class DecodeEngine:
                 ldq = self.qkvq.stride(0)
 
                 def do_append(li=li, sel=sel, ldq=ldq):
+                    if spec_wait and self.qkv_db:
+                        # idx / n / slot tables of li (the append's fetch metadata and the
+                        # attention read them); the GEMM above wrote the other parity's qspec
+                        C.wait_event(self.ev_sel[li])
                     if AP is not C:
                         self.ev_qkv[li].record(C)
                         AP.wait_event(self.ev_qkv[li])
@@ -1625,6 +1647,7 @@ def run(model, config: RunConfig, *, prompts=None, **kw):
         prompts = np.stack([np.random.default_rng(config.prompt_seed + b)
                             .standard_normal((config.prompt_len, D)).astype(np.float32)
                             for b in range(config.batch)])
+    kw.setdefault("record_trace", True)     # the reference's run() always records its LayerRecords
     eng = DecodeEngine(model, config, **kw)
     try:
         eng.prefill(prompts)
