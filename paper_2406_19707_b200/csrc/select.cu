@@ -9,8 +9,6 @@
 //   { t : key > P }  U  { first `need` t in index order with key == P }
 // in ascending row order -- the order the host-pool gather wants (ascending
 // rows keep the PCIe reads page-local: 52.7 vs 35 GB/s measured).
-#include <cooperative_groups.h>
-
 #include "common.cuh"
 
 namespace ig {
@@ -469,359 +467,6 @@ select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ coun
   }
 }
 
-// ---------------------------------------------------------------------------
-// Long rows (C4: 32K scores per (b, h), only B x Hg = 128 rows for 148 SMs):
-// the same value-bin select spread over a cluster of kSelCl CTAs per row.  CTA
-// c of the cluster owns rows [c span, (c+1) span); the min / max, the 2048-bin
-// histogram, the boundary-bin candidates (or the radix digit histograms), the
-// per-CTA taken / tie counts are combined through distributed shared memory,
-// so every CTA takes the same decisions, and each emits its own slice at the
-// offset of the taken rows before it (ascending order is kept).
-// ---------------------------------------------------------------------------
-constexpr int kSelCl = 8;
-constexpr int kSelClThreads = 512;
-constexpr int kSelClMinRows = 16384;         // below: one CTA per row (select_kernel)
-
-struct ClShared {
-  uint32_t hist[kBins];       // this CTA's slice
-  uint32_t ghist[kBins];      // the row (sum over the cluster)
-  uint32_t cand_key[kCandMax];
-  int32_t cand_t[kCandMax];
-  uint32_t kmin[kSelWarps], kmax[kSelWarps];
-  int scan[kSelWarps];
-  int warp_a[kSelWarps], warp_b[kSelWarps];
-  uint32_t lkmin, lkmax;      // slice min / max keys
-  int ncand;                  // slice candidates (mode 1)
-  int taken, eqc;             // slice: rows taken (before the tie quota), rows == P (mode 2)
-  int bstar, need, m;
-  uint32_t rhist[256];        // radix digit histogram of the slice
-  uint32_t rprefix;
-  int rneed;
-};
-
-__global__ void __launch_bounds__(kSelClThreads)
-select_cluster_kernel(const float* __restrict__ scores, const int32_t* __restrict__ count_sum,
-                      const ig_step_state* __restrict__ st, int Hg, int H_total, int S_max, int cap_max,
-                      double cap_ratio, int min_select, int32_t* __restrict__ idx,
-                      int32_t* __restrict__ n_out, int32_t* __restrict__ err_flag) {
-  namespace cg = cooperative_groups;
-  constexpr int THREADS = kSelClThreads, NW = THREADS / kWarp, PER = kBins / THREADS;
-  cg::cluster_group cl = cg::this_cluster();
-  __shared__ ClShared sh;
-  extern __shared__ uint32_t bits[];            // take bitmap of the slice (mode 1)
-  const int c = (int)cl.block_rank();
-  const int b = blockIdx.y, h = blockIdx.x / kSelCl;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int s = st->s_len;
-  const long long sum = count_sum[b];
-  long long n = (2 * sum + H_total) / (2LL * H_total);
-  const long long cap = max((long long)floor(cap_ratio * (double)s), (long long)min_select);
-  n = min(max(n, (long long)min_select), cap);
-  n = min(n, (long long)s);
-  int nn = (int)n;
-  if (nn > cap_max) {
-    if (tid == 0 && c == 0) *reinterpret_cast<volatile int32_t*>(err_flag) = 1;
-    nn = cap_max;
-  }
-  if (h == 0 && c == 0 && tid == 0) n_out[b] = nn;
-  const size_t bh = (size_t)b * Hg + h;
-  const float* row = scores + bh * S_max;
-  int32_t* out = idx + bh * cap_max;
-  const int span = ((s + kSelCl - 1) / kSelCl + 127) & ~127;
-  const int c_lo = min(s, c * span), c_hi = min(s, c_lo + span);
-  if (nn >= s) {                       // every row (the same decision in every CTA)
-    for (int t = c_lo + tid; t < c_hi; t += THREADS) out[t] = t;
-    return;
-  }
-  if (nn <= 0) return;
-
-  // ---- P0: min / max keys of the slice, then of the row
-  uint32_t kmin = 0xffffffffu, kmax = 0u;
-  for (int t = c_lo + tid * 4; t < c_hi; t += THREADS * 4) {
-    const float4 v = row4(row, t);
-    const float x[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (t + i < c_hi) {
-        const uint32_t k = order_key(x[i]);
-        kmin = min(kmin, k);
-        kmax = max(kmax, k);
-      }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-  }
-  if (lane == 0) { sh.kmin[w] = kmin; sh.kmax[w] = kmax; }
-  for (int i = tid; i < kBins; i += THREADS) sh.hist[i] = 0;
-  __syncthreads();
-  if (tid == 0) {
-    uint32_t a0 = sh.kmin[0], a1 = sh.kmax[0];
-    for (int i = 1; i < NW; ++i) { a0 = min(a0, sh.kmin[i]); a1 = max(a1, sh.kmax[i]); }
-    sh.lkmin = a0;
-    sh.lkmax = a1;
-  }
-  cl.sync();
-  kmin = 0xffffffffu;
-  kmax = 0u;
-  for (int r = 0; r < kSelCl; ++r) {
-    const ClShared* o = cl.map_shared_rank(&sh, r);
-    kmin = min(kmin, o->lkmin);
-    kmax = max(kmax, o->lkmax);
-  }
-  const float hi = key_to_float(kmax), lo = key_to_float(kmin);
-  float scale = (float)kBins / (hi - lo);
-  if (!(scale < 1e30f)) scale = 0.f;
-
-  // ---- P1: slice histogram -> row histogram -> boundary bin
-  for (int t = c_lo + tid * 4; t < c_hi; t += THREADS * 4) {
-    const float4 v = row4(row, t);
-    const float x[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (t + i < c_hi) atomicAdd(&sh.hist[vbin(x[i], hi, scale)], 1u);
-  }
-  cl.sync();
-  for (int i = tid; i < kBins; i += THREADS) {
-    uint32_t g = 0;
-    for (int r = 0; r < kSelCl; ++r) g += cl.map_shared_rank(sh.hist, r)[i];
-    sh.ghist[i] = g;
-  }
-  __syncthreads();
-  {
-    int cc[PER], tot = 0;
-#pragma unroll
-    for (int i = 0; i < PER; ++i) { cc[i] = (int)sh.ghist[tid * PER + i]; tot += cc[i]; }
-    const int incl = block_incl_scan(tot, sh.scan);
-    const int excl = incl - tot;
-    if (excl < nn && incl >= nn) {
-      int cum = excl;
-#pragma unroll
-      for (int i = 0; i < PER; ++i) {
-        if (cum + cc[i] >= nn) {
-          sh.bstar = tid * PER + i;
-          sh.need = nn - cum;
-          sh.m = cc[i];
-          break;
-        }
-        cum += cc[i];
-      }
-    }
-    if (tid == 0) sh.ncand = 0;
-  }
-  const int slice_words = (c_hi - c_lo + 31) / 32;
-  for (int i = tid; i < slice_words; i += THREADS) bits[i] = 0;
-  __syncthreads();
-  const int bstar = sh.bstar, need = sh.need, m = sh.m;
-  const int mode = (m == need) ? 0 : (m <= kCandMax ? 1 : 2);
-  // warp w owns rows [t_lo, t_hi) of the slice
-  const int wspan = ((c_hi - c_lo + NW - 1) / NW + 127) & ~127;
-  const int t_lo = min(c_hi, c_lo + w * wspan), t_hi = min(c_hi, t_lo + wspan);
-
-  // ---- P2: radix resolution of b* over the whole row (mode 2)
-  uint32_t P = 0u;
-  int need_eq = 0;
-  if (mode == 2) {
-    uint32_t prefix = 0u, mask = 0u;
-    int nd = need;
-    for (int pass = 0; pass < 4; ++pass) {
-      const int shift = 24 - 8 * pass;
-      for (int i = tid; i < 256; i += THREADS) sh.rhist[i] = 0;
-      __syncthreads();
-      for (int t0 = c_lo; t0 < c_hi; t0 += THREADS) {
-        const int t = t0 + tid;
-        bool live = false;
-        uint32_t bin = 0;
-        if (t < c_hi) {
-          const float x = __ldcg(row + t);
-          const uint32_t key = order_key(x);
-          live = vbin(x, hi, scale) == bstar && (key & mask) == prefix;
-          bin = (key >> shift) & 255u;
-        }
-        const unsigned act = __ballot_sync(0xffffffffu, live);
-        if (live) {
-          const unsigned peers = __match_any_sync(act, bin);
-          if ((__ffs(peers) - 1) == lane) atomicAdd(&sh.rhist[bin], (uint32_t)__popc(peers));
-        }
-      }
-      cl.sync();                      // every slice's digit histogram is complete
-      if (w == 0) {
-        // pick_digit over the row's histogram (sum of the cluster's), lane L owns
-        // bins 255-8L .. 248-8L
-        int cc[8], tot = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int bin = 255 - 8 * lane - i;
-          uint32_t g = 0;
-          for (int r = 0; r < kSelCl; ++r) g += cl.map_shared_rank(sh.rhist, r)[bin];
-          cc[i] = (int)g;
-          tot += cc[i];
-        }
-        int incl = tot;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const int excl = incl - tot;
-        const unsigned hitmask = __ballot_sync(0xffffffffu, excl < nd && incl >= nd);
-        const int src = __ffs(hitmask) - 1;
-        if (lane == src) {
-          int cum = excl, bin = 255 - 8 * lane;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (cum + cc[i] >= nd) { bin = 255 - 8 * lane - i; break; }
-            cum += cc[i];
-          }
-          sh.rprefix = prefix | ((uint32_t)bin << shift);
-          sh.rneed = nd - cum;
-        }
-      }
-      cl.sync();                      // remote reads done before the next pass clears
-      prefix = sh.rprefix;
-      nd = sh.rneed;
-      mask |= 255u << shift;
-    }
-    P = prefix;
-    need_eq = nd;
-  }
-
-  // ---- per-warp counts of the slice (+ mode 1 candidate gather)
-  int a = 0, e = 0;
-  for (int t = t_lo + lane * 4; t < t_hi; t += 128) {
-    const float4 v = row4(row, t);
-    const float x[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (t + i >= t_hi) break;
-      const int bn = vbin(x[i], hi, scale);
-      if (bn < bstar) {
-        ++a;
-      } else if (bn == bstar) {
-        if (mode == 0) {
-          ++a;
-        } else if (mode == 1) {
-          const int slot = atomicAdd(&sh.ncand, 1);
-          sh.cand_key[slot] = order_key(x[i]);
-          sh.cand_t[slot] = t + i;
-        } else {
-          const uint32_t k = order_key(x[i]);
-          a += k > P;
-          e += k == P;
-        }
-      }
-    }
-  }
-  a = warp_sum(a);
-  e = warp_sum(e);
-  if (mode == 1) {
-    // rank this slice's candidates against every candidate of the row:
-    // (key desc, row asc) -- the reference's stable order
-    cl.sync();                        // every slice's candidates are gathered
-    const int mine = sh.ncand;
-    for (int i = tid; i < mine; i += THREADS) {
-      const uint32_t ki = sh.cand_key[i];
-      const int ti = sh.cand_t[i];
-      int rank = 0;
-      for (int r = 0; r < kSelCl; ++r) {
-        const ClShared* o = cl.map_shared_rank(&sh, r);
-        const int nr = o->ncand;
-        for (int j = 0; j < nr; ++j) {
-          const uint32_t kj = o->cand_key[j];
-          rank += (kj > ki) || (kj == ki && o->cand_t[j] < ti);
-        }
-      }
-      if (rank < need) atomicOr(&bits[(ti - c_lo) >> 5], 1u << ((ti - c_lo) & 31));
-    }
-    __syncthreads();
-    int tk = 0;
-    for (int wd = ((t_lo - c_lo) >> 5) + lane; wd < (t_hi - c_lo + 31) >> 5; wd += 32) tk += __popc(bits[wd]);
-    a += warp_sum(tk);
-  }
-  if (lane == 0) { sh.warp_a[w] = a; sh.warp_b[w] = e; }
-  __syncthreads();
-  if (tid == 0) {
-    int ta = 0, te = 0;
-    for (int i = 0; i < NW; ++i) { ta += sh.warp_a[i]; te += sh.warp_b[i]; }
-    sh.taken = ta;
-    sh.eqc = te;
-  }
-  cl.sync();
-  // rows taken by the slices before mine (their tie quota included), ties before mine
-  int base = 0, eq_before = 0;
-  for (int r = 0; r < c; ++r) {
-    const ClShared* o = cl.map_shared_rank(&sh, r);
-    const int ee = min(o->eqc, max(0, need_eq - eq_before));
-    eq_before += o->eqc;
-    base += o->taken + ee;
-  }
-
-  // ---- P3: ascending emission of the slice
-  int out_off = base;
-  for (int i = 0; i < w; ++i) {
-    const int ee = min(sh.warp_b[i], max(0, need_eq - eq_before));
-    eq_before += sh.warp_b[i];
-    out_off += sh.warp_a[i] + ee;
-  }
-  for (int t0 = t_lo; t0 < t_hi; t0 += 128) {
-    const int t = t0 + lane * 4;
-    float x[4] = {0.f, 0.f, 0.f, 0.f};
-    if (t < t_hi) {
-      const float4 v = row4(row, t);
-      x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
-    }
-    bool sure[4], eq[4];
-    int ns = 0, ne = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      sure[i] = eq[i] = false;
-      if (t + i < t_hi) {
-        const int bn = vbin(x[i], hi, scale);
-        if (bn < bstar) {
-          sure[i] = true;
-        } else if (bn == bstar) {
-          if (mode == 0) sure[i] = true;
-          else if (mode == 1) sure[i] = (bits[(t + i - c_lo) >> 5] >> ((t + i - c_lo) & 31)) & 1u;
-          else {
-            const uint32_t k = order_key(x[i]);
-            sure[i] = k > P;
-            eq[i] = k == P;
-          }
-        }
-      }
-      ne += eq[i];
-    }
-    int e_incl = ne;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, e_incl, o);
-      if (lane >= o) e_incl += y;
-    }
-    int e_run = eq_before + e_incl - ne;
-    bool take[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      take[i] = sure[i] || (eq[i] && e_run < need_eq);
-      e_run += eq[i];
-      ns += take[i];
-    }
-    int incl = ns;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    int pos = out_off + incl - ns;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (take[i]) out[pos++] = t + i;
-    out_off += __shfl_sync(0xffffffffu, incl, 31);
-    eq_before += __shfl_sync(0xffffffffu, e_incl, 31);
-  }
-  cl.sync();                          // no CTA leaves while the others read its shared memory
-}
-
 // Rewrite idx[0:n) of each (b, h) into stable descending-score order
 // (ties -> lower index), the order topk_indices returns.  O(n^2) rank sort in
 // shared memory: drop-in shim only, never on the engine path.
@@ -870,31 +515,6 @@ extern "C" int ig_select(const float* scores, const int32_t* count_sum, const ig
       !err_flag)
     return IG_EINVAL;
   if (S_max > kSelMaxRows) return IG_EINVAL;
-  static const bool no_cluster = [] {
-    const char* e = getenv("IG_SELECT_CLUSTER");
-    return e && atoi(e) == 0;
-  }();
-  if (S_max >= kSelClMinRows && !no_cluster) {
-    // a cluster of kSelCl CTAs per (b, h) row; bitmap of one slice
-    const int span = ((S_max + kSelCl - 1) / kSelCl + 127) & ~127;
-    const size_t csmem = (size_t)(span + 31) / 32 * 4;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kSelCl * Hg, B);
-    cfg.blockDim = dim3(kSelClThreads);
-    cfg.dynamicSmemBytes = csmem;
-    cfg.stream = (cudaStream_t)stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = kSelCl;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    IG_CUDA_STATUS(cudaLaunchKernelEx(&cfg, select_cluster_kernel, scores, count_sum, st, Hg, H_total, S_max,
-                                      cap_max, cap_ratio, min_select, idx, n_out, err_flag));
-    IG_LAUNCH_STATUS();
-    return IG_OK;
-  }
   const size_t smem = (size_t)(S_max + 31) / 32 * 4;  // the take bitmap
   auto kern = S_max > kSelLongRows ? select_kernel<kSelThreadsLong> : select_kernel<kSelThreads>;
   const int threads = S_max > kSelLongRows ? kSelThreadsLong : kSelThreads;
