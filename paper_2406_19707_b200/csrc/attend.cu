@@ -1215,11 +1215,11 @@ attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restric
 // (round 1): register-fed 2.84 TB/s vs TMA-fed 2.39 TB/s -- the per-row math
 // (f16 unpack + shuffle reductions), not the feed, bounds this kernel, so
 // the register-fed loop stays the default.
-// 'c' (default: tcgen05, attend_tc05.cu), 'm' (mma.sync), 'r' (register-fed), 't' (TMA-fed)
+// 'm' (default: mma.sync), 'c' (tcgen05, attend_tc05.cu), 'r' (register-fed), 't' (TMA-fed)
 inline char attend_impl() {
   static const char impl = [] {
     const char* v = getenv("IG_ATTEND_IMPL");
-    return v && (v[0] == 'r' || v[0] == 't' || v[0] == 'm') ? v[0] : 'c';
+    return v && (v[0] == 'r' || v[0] == 't' || v[0] == 'c') ? v[0] : 'm';
   }();
   return impl;
 }
@@ -1237,16 +1237,12 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
                   const ig_step_state* st, int Hg, int d, int cap, float sqrt_d, int max_chunks,
                   float* partial, int32_t* tickets, float* out, int ldo) {
   if constexpr (sizeof(T) == 2) {
-    // tcgen05 (attend_tc05.cu) for row sets above 2K rows (layer 0's full
-    // mirror, long-context selections: 6.07 vs 5.94 TB/s at 4K rows), the
-    // mma.sync warp-persistent kernel below (68 vs 73 us at C3's 819 rows,
-    // tools/attend_trace.py); IG_ATTEND_IMPL=c forces tcgen05 everywhere.
-    // -1 from the launcher: not applicable here.
-    static const bool force_c = [] {
-      const char* v = getenv("IG_ATTEND_IMPL");
-      return v && v[0] == 'c';
-    }();
-    if (d == 128 && attend_impl() == 'c' && (cap > 2048 || force_c)) {
+    // tcgen05 (attend_tc05.cu) only on request (IG_ATTEND_IMPL=c): it measured
+    // 6.07 vs 5.94 TB/s on 640 (b, h) x 4K-row sets but 73 vs 68 us at C3's 819-row
+    // sets and 105 vs 84 us at C4 (128 (b, h) x 6.5K rows), so the mma.sync
+    // kernels below stay the default (profiles/r02o_*, r02x_*).  -1 from the
+    // launcher: not applicable here.
+    if (d == 128 && attend_impl() == 'c') {
       const int rc = attend_tc05_launch(std::is_same<T, __half>::value ? IG_ELT_F16 : IG_ELT_BF16, s, q, ldq, k_cur,
                                         v_cur, ldkv, stage, idx, n, rows_bh, pos, st, (int)grid.z, Hg, cap, sqrt_d,
                                         max_chunks, partial, tickets, out, ldo);

@@ -587,46 +587,64 @@ def test_attend_wp_variants_match_default(env):
         np.testing.assert_allclose(res["variant"], res["default"], rtol=1e-5, atol=1e-6)
 
 
+_LONG_ROWS_CODE = """
+import sys, ctypes, numpy as np, torch
+from paper_2406_19707_b200 import _lib
+elt = sys.argv[2]
+B, Hg, d, cap = 2, 3, 128, 4100
+g = torch.Generator(device="cuda"); g.manual_seed(21)
+T = torch.float16 if elt == "f16" else torch.bfloat16
+q = torch.randn(B, 3 * Hg * d, device="cuda", generator=g)
+stage = torch.full((B, Hg, cap, 2 * d), float("nan"), device="cuda").to(T)
+used = torch.tensor([[4100, 2049, 0], [3000, 129, 4096]], dtype=torch.int32, device="cuda")
+for b in range(B):
+    for h in range(Hg):
+        n = int(used[b, h])
+        stage[b, h, :n] = (2 * torch.randn(n, 2 * d, device="cuda", generator=g)).to(T)
+slot = torch.arange(cap, device="cuda", dtype=torch.int32).repeat(B, Hg, 1).contiguous()
+slot[:, :, 3::11] = -1
+pos = torch.full((B, Hg), 7, dtype=torch.int32, device="cuda")
+st = torch.zeros(8, dtype=torch.int32, device="cuda")
+pf, tk = ctypes.c_size_t(), ctypes.c_size_t()
+_lib.call("ig_attend_scratch", B, Hg, d, cap, ctypes.byref(pf), ctypes.byref(tk), kernels=0)
+part = torch.empty(pf.value, device="cuda")
+tick = torch.zeros(tk.value, dtype=torch.int32, device="cuda")
+outs = []
+for _ in range(2):
+    out = torch.empty(B, Hg * d, device="cuda")
+    _lib.call("ig_attend_slots", q.data_ptr(), 3 * Hg * d, q.data_ptr() + 4 * Hg * d, q.data_ptr() + 8 * Hg * d,
+              3 * Hg * d, stage.data_ptr(), _lib.ELT[elt], slot.data_ptr(), used.data_ptr(), pos.data_ptr(),
+              st.data_ptr(), B, Hg, d, cap, part.data_ptr(), tick.data_ptr(), out.data_ptr(), Hg * d,
+              _lib.stream_handle())
+    outs.append(out.cpu().numpy())
+assert not tick.any()
+np.savez(sys.argv[1], o0=outs[0], o1=outs[1], q=q.double().cpu().numpy(), stage=stage.double().cpu().numpy(),
+         used=used.cpu().numpy(), slot=slot.cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("impl", ["c", "mma"])
 @pytest.mark.parametrize("elt", ["f16", "bf16"])
-def test_attend_tc05_long_rows_vs_float64(elt):
-    """The tcgen05 attention (csrc/attend_tc05.cu, the default above 2K rows)
-    over long slot tables: (b, h) row sets split over several CTAs (partial
-    slots + ticket merges), an empty set (output = the current row's v),
-    excluded rows (empty slots, pos), NaN rows past each count; vs float64."""
-    import ctypes
-    import torch
-    from paper_2406_19707_b200 import _lib
-    B, Hg, d, cap = 2, 3, 128, 4100
-    g = torch.Generator(device="cuda")
-    g.manual_seed(21)
-    T = torch.float16 if elt == "f16" else torch.bfloat16
-    q = torch.randn(B, 3 * Hg * d, device="cuda", generator=g)
-    stage = torch.full((B, Hg, cap, 2 * d), float("nan"), device="cuda").to(T)
-    used = torch.tensor([[4100, 2049, 0], [3000, 129, 4096]], dtype=torch.int32, device="cuda")
-    for b in range(B):
-        for h in range(Hg):
-            n = int(used[b, h])
-            stage[b, h, :n] = (2 * torch.randn(n, 2 * d, device="cuda", generator=g)).to(T)
-    slot = torch.arange(cap, device="cuda", dtype=torch.int32).repeat(B, Hg, 1).contiguous()
-    slot[:, :, 3::11] = -1
-    pos = torch.full((B, Hg), 7, dtype=torch.int32, device="cuda")
-    st = torch.zeros(8, dtype=torch.int32, device="cuda")
-    pf, tk = ctypes.c_size_t(), ctypes.c_size_t()
-    _lib.call("ig_attend_scratch", B, Hg, d, cap, ctypes.byref(pf), ctypes.byref(tk), kernels=0)
-    part = torch.empty(pf.value, device="cuda")
-    tick = torch.zeros(tk.value, dtype=torch.int32, device="cuda")
-    outs = []
-    for _ in range(2):
-        out = torch.empty(B, Hg * d, device="cuda")
-        _lib.call("ig_attend_slots", q.data_ptr(), 3 * Hg * d, q.data_ptr() + 4 * Hg * d, q.data_ptr() + 8 * Hg * d,
-                  3 * Hg * d, stage.data_ptr(), _lib.ELT[elt], slot.data_ptr(), used.data_ptr(), pos.data_ptr(),
-                  st.data_ptr(), B, Hg, d, cap, part.data_ptr(), tick.data_ptr(), out.data_ptr(), Hg * d,
-                  _lib.stream_handle())
-        outs.append(out.cpu().numpy())
-    assert not tick.any()                                  # tickets left zeroed
-    np.testing.assert_array_equal(outs[0], outs[1])        # deterministic merges
-    qn = q.double().cpu().numpy()
-    stg = stage.double().cpu().numpy()
+def test_attend_long_rows_vs_float64(elt, impl):
+    """Long slot tables (4K rows per (b, h)) through the tcgen05 attention
+    (IG_ATTEND_IMPL=c: csrc/attend_tc05.cu -- (b, h) row sets split over
+    several CTAs with partial slots + ticket merges) and the default mma.sync
+    kernel: an empty set (output = the current row's v), excluded rows (empty
+    slots, pos), NaN rows past each count; tickets left zeroed, bit-identical
+    on repeat, vs float64."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    f = os.path.join(tempfile.mkdtemp(), "o.npz")
+    r = subprocess.run([sys.executable, "-c", _LONG_ROWS_CODE, f, elt], env=dict(os.environ, IG_ATTEND_IMPL=impl),
+                       capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-2000:]
+    z = np.load(f)
+    np.testing.assert_array_equal(z["o0"], z["o1"])        # deterministic merges
+    B, Hg, d = 2, 3, 128
+    qn, stg, used, slot = z["q"], z["stage"], z["used"], z["slot"]
     for b in range(B):
         for h in range(Hg):
             n = int(used[b, h])
@@ -635,5 +653,5 @@ def test_attend_tc05_long_rows_vs_float64(elt):
             V = np.concatenate([stg[b, h, rows, d:], qn[b, 2 * Hg * d + h * d:2 * Hg * d + (h + 1) * d][None]])
             lg = K @ qn[b, h * d:(h + 1) * d] / np.sqrt(d)
             w = np.exp(lg - lg.max())
-            np.testing.assert_allclose(outs[0][b, h * d:(h + 1) * d], (w / w.sum()) @ V, rtol=2e-5, atol=2e-5,
+            np.testing.assert_allclose(z["o0"][b, h * d:(h + 1) * d], (w / w.sum()) @ V, rtol=2e-5, atol=2e-5,
                                        err_msg=f"b{b} h{h} n{n}")
