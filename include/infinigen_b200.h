@@ -118,6 +118,14 @@ int ig_order_by_score(const float* scores, const int32_t* n, int B, int Hg,
 
 /* Generic top-k per row (ties -> lower index), ascending output.  Used for
  * build_partial's column choice (speculation.py:41-58).                   */
+/* ig_select + ig_resident_plan of the same (b, h) in one launch (the plan runs
+ * in the select's CTA on the selection it just wrote): same arguments as the
+ * two calls, same results. */
+int ig_select_plan(const float* scores, const int32_t* count_sum, const ig_step_state* st, int B,
+                   int Hg, int H_total, int S_max, int cap_max, double cap_ratio, int min_select,
+                   int32_t* idx, int32_t* n_out, int32_t* err_flag, const int32_t* pos_prev,
+                   int32_t* slot_id, int32_t* slot_used, int32_t* frow, int32_t* fslot,
+                   int32_t* fcount, int64_t* moved_rows, void* stream);
 int ig_topk_rows(const float* values, int rows, int len, int k, int32_t* idx_out,
                  void* stream);
 

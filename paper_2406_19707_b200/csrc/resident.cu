@@ -21,37 +21,9 @@
 //                     appended row goes to its HBM mirror in the same step
 //   ig_attend_slots   (attend.cu) attention over the slot table
 #include "common.cuh"
+#include "plan.cuh"
 
 namespace ig {
-
-constexpr int kPlanThreads = 256;
-
-__device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ a, int n, int v) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (a[mid] < v) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
-// Exclusive block-wide prefix of `flag` (ballot per warp, warp totals in
-// smem); `total` receives the block total.  Every thread must call it.
-__device__ __forceinline__ int block_rank(bool flag, int* wsum, int& total) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const unsigned bal = __ballot_sync(0xffffffffu, flag);
-  __syncthreads();                     // previous call's wsum reads are done
-  if (lane == 0) wsum[w] = __popc(bal);
-  __syncthreads();
-  int before = 0;
-  total = 0;
-  for (int i = 0; i < nw; ++i) {
-    const int c = wsum[i];
-    before += i < w ? c : 0;
-    total += c;
-  }
-  return before + __popc(bal & ((1u << lane) - 1u));
-}
 
 __global__ void __launch_bounds__(kPlanThreads)
 resident_plan_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ n_in,
@@ -63,64 +35,10 @@ resident_plan_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict_
   int32_t* freelist = plan_smem;                                   // [cap]
   uint8_t* matched = reinterpret_cast<uint8_t*>(plan_smem + cap);  // [cap]
   __shared__ int wsum[kPlanThreads / kWarp];
-  const int b = blockIdx.y, h = blockIdx.x, tid = threadIdx.x;
+  const int b = blockIdx.y, h = blockIdx.x;
   const size_t bh = (size_t)b * Hg + h;
-  const int n = n_in[b];
-  const int U = slot_used[bh];
-  const int pp = pos_prev ? pos_prev[bh] : -1;
-  int32_t* ids = slot_id + bh * cap;
-  const int32_t* sel = idx + bh * cap;
-
-  for (int p = tid; p < n; p += blockDim.x) matched[p] = 0;
-  __syncthreads();
-  // 1. keep the slots whose row is still selected (and was not overwritten)
-  for (int j = tid; j < U; j += blockDim.x) {
-    const int id = ids[j];
-    bool keep = false;
-    if (id >= 0 && id != pp) {
-      const int p = lower_bound_i32(sel, n, id);
-      if (p < n && sel[p] == id) {
-        matched[p] = 1;
-        keep = true;
-      }
-    }
-    if (!keep && id != -1) ids[j] = -1;
-  }
-  __syncthreads();
-  // 2. free slots below U, ascending
-  int nfree = 0;
-  for (int base = 0; base < U; base += blockDim.x) {
-    const int j = base + tid;
-    const bool f = j < U && ids[j] < 0;
-    int tot;
-    const int r = block_rank(f, wsum, tot);
-    if (f) freelist[nfree + r] = j;
-    nfree += tot;
-  }
-  __syncthreads();
-  // 3. rows that entered the selection (ascending) take the free slots in
-  //    order, then fresh slots from U up
-  int nun = 0;
-  for (int base = 0; base < n; base += blockDim.x) {
-    const int p = base + tid;
-    const bool f = p < n && !matched[p];
-    int tot;
-    const int r = block_rank(f, wsum, tot);
-    if (f) {
-      const int k = nun + r;
-      const int slot = k < nfree ? freelist[k] : U + (k - nfree);
-      const int row = sel[p];
-      ids[slot] = row;
-      frow[bh * cap + k] = row;
-      fslot[bh * cap + k] = slot;
-    }
-    nun += tot;
-  }
-  if (tid == 0) {
-    fcount[bh] = nun;
-    slot_used[bh] = nun > nfree ? U + (nun - nfree) : U;
-    if (moved_rows && nun) atomicAdd(moved_rows, (unsigned long long)nun);
-  }
+  plan_row(idx + bh * cap, n_in[b], pos_prev ? pos_prev[bh] : -1, slot_id + bh * cap, slot_used + bh,
+           frow + bh * cap, fslot + bh * cap, fcount + bh, moved_rows, freelist, matched, wsum);
 }
 
 constexpr int kSlotFetchThreads = 128;

@@ -10,6 +10,7 @@
 // in ascending row order -- the order the host-pool gather wants (ascending
 // rows keep the PCIe reads page-local: 52.7 vs 35 GB/s measured).
 #include "common.cuh"
+#include "plan.cuh"
 
 namespace ig {
 
@@ -212,16 +213,16 @@ __device__ __forceinline__ float4 row4(const float* row, int t) {
   return __ldcg(reinterpret_cast<const float4*>(row + t));
 }
 
+// The select of one (b, h) row; returns the number of rows written to
+// idx[bh][0:n) (ascending).
 template <int THREADS>
-__global__ void __launch_bounds__(THREADS)
-select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ count_sum,
-              const ig_step_state* __restrict__ st, int Hg, int H_total, int S_max, int cap_max,
-              double cap_ratio, int min_select, int32_t* __restrict__ idx,
-              int32_t* __restrict__ n_out, int32_t* __restrict__ err_flag) {
+__device__ __forceinline__ int select_row(const float* __restrict__ scores, const int32_t* __restrict__ count_sum,
+                                          const ig_step_state* __restrict__ st, int Hg, int H_total, int S_max,
+                                          int cap_max, double cap_ratio, int min_select, int32_t* __restrict__ idx,
+                                          int32_t* __restrict__ n_out, int32_t* __restrict__ err_flag,
+                                          BinShared& sh, uint32_t* __restrict__ bits) {
   constexpr int NW = THREADS / kWarp;
   constexpr int PER = kBins / THREADS;
-  __shared__ BinShared sh;
-  extern __shared__ uint32_t bits[];            // take bitmap, ceil(S_max / 32) words
   const int b = blockIdx.y, h = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int s = st->s_len;
@@ -244,9 +245,9 @@ select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ coun
   int32_t* out = idx + bh * cap_max;
   if (nn >= s) {
     for (int t = tid; t < s; t += THREADS) out[t] = t;
-    return;
+    return s;
   }
-  if (nn <= 0) return;
+  if (nn <= 0) return 0;
 
   // ---- P0: row min / max (order keys)
   uint32_t kmin = 0xffffffffu, kmax = 0u;
@@ -465,6 +466,34 @@ select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ coun
     out_off += __shfl_sync(0xffffffffu, incl, 31);
     eq_before += __shfl_sync(0xffffffffu, e_incl, 31);
   }
+  return nn;
+}
+
+
+// ig_select (plan == false) / ig_select_plan (plan == true: the resident plan
+// of the same (b, h) runs in the same CTA on the selection just written --
+// one launch and one dependent hop fewer on the speculation chain)
+template <int THREADS, bool PLAN>
+__global__ void __launch_bounds__(THREADS)
+select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ count_sum,
+              const ig_step_state* __restrict__ st, int Hg, int H_total, int S_max, int cap_max,
+              double cap_ratio, int min_select, int32_t* __restrict__ idx,
+              int32_t* __restrict__ n_out, int32_t* __restrict__ err_flag, const int32_t* __restrict__ pos_prev,
+              int32_t* __restrict__ slot_id, int32_t* __restrict__ slot_used, int32_t* __restrict__ frow,
+              int32_t* __restrict__ fslot, int32_t* __restrict__ fcount,
+              unsigned long long* __restrict__ moved_rows) {
+  __shared__ BinShared sh;
+  extern __shared__ uint32_t bits[];            // take bitmap, ceil(S_max / 32) words (+ plan scratch)
+  const int n = select_row<THREADS>(scores, count_sum, st, Hg, H_total, S_max, cap_max, cap_ratio, min_select,
+                                    idx, n_out, err_flag, sh, bits);
+  if constexpr (PLAN) {
+    const size_t bh = (size_t)blockIdx.y * Hg + blockIdx.x;
+    int32_t* freelist = reinterpret_cast<int32_t*>(bits + (S_max + 31) / 32);
+    uint8_t* matched = reinterpret_cast<uint8_t*>(freelist + cap_max);
+    __syncthreads();                  // the selection (global) and the bitmap reads are done
+    plan_row(idx + bh * cap_max, n, pos_prev ? pos_prev[bh] : -1, slot_id + bh * cap_max, slot_used + bh,
+             frow + bh * cap_max, fslot + bh * cap_max, fcount + bh, moved_rows, freelist, matched, sh.scan);
+  }
 }
 
 // Rewrite idx[0:n) of each (b, h) into stable descending-score order
@@ -505,27 +534,61 @@ topk_rows_kernel(const float* __restrict__ values, int len, int k, int32_t* __re
 
 }  // namespace ig
 
-extern "C" int ig_select(const float* scores, const int32_t* count_sum, const ig_step_state* st,
-                         int B, int Hg, int H_total, int S_max, int cap_max, double cap_ratio,
-                         int min_select, int32_t* idx, int32_t* n_out, int32_t* err_flag,
+namespace ig {
+static int select_launch(const float* scores, const int32_t* count_sum, const ig_step_state* st, int B, int Hg,
+                         int H_total, int S_max, int cap_max, double cap_ratio, int min_select, int32_t* idx,
+                         int32_t* n_out, int32_t* err_flag, const int32_t* pos_prev, int32_t* slot_id,
+                         int32_t* slot_used, int32_t* frow, int32_t* fslot, int32_t* fcount, int64_t* moved_rows,
                          void* stream) {
-  using namespace ig;
   if (B < 1 || Hg < 1 || H_total < Hg || S_max < 1 || cap_max < 1 || !(cap_ratio > 0) ||
       cap_ratio > 1 || min_select < 1 || !scores || !count_sum || !st || !idx || !n_out ||
       !err_flag)
     return IG_EINVAL;
   if (S_max > kSelMaxRows) return IG_EINVAL;
-  const size_t smem = (size_t)(S_max + 31) / 32 * 4;  // the take bitmap
-  auto kern = S_max > kSelLongRows ? select_kernel<kSelThreadsLong> : select_kernel<kSelThreads>;
-  const int threads = S_max > kSelLongRows ? kSelThreadsLong : kSelThreads;
+  const bool plan = slot_id != nullptr;
+  if (plan && (!slot_used || !frow || !fslot || !fcount)) return IG_EINVAL;
+  // the take bitmap (+ the plan's free list and match flags)
+  const size_t smem = (size_t)(S_max + 31) / 32 * 4 + (plan ? (size_t)cap_max * 5 : 0);
+  if (smem > 200 * 1024) return IG_EINVAL;
+  // IG_SELECT_THREADS=256|512 for rows up to kSelLongRows (A/B: how many CTAs fit one wave)
+  static const int short_threads = [] {
+    const char* e = getenv("IG_SELECT_THREADS");
+    return e && atoi(e) == 256 ? 256 : kSelThreads;
+  }();
+  const int threads = S_max > kSelLongRows ? kSelThreadsLong : short_threads;
+  auto pick = [&](auto k512, auto k256, auto k1024) {
+    return S_max > kSelLongRows ? k1024 : (short_threads == 256 ? k256 : k512);
+  };
+  auto kern = plan ? pick(select_kernel<kSelThreads, true>, select_kernel<256, true>,
+                          select_kernel<kSelThreadsLong, true>)
+                   : pick(select_kernel<kSelThreads, false>, select_kernel<256, false>,
+                          select_kernel<kSelThreadsLong, false>);
   if (smem > 16 * 1024)  // dynamic + static (~25 KB) must fit: opt in early
-    IG_CUDA_STATUS(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)smem));
+    IG_CUDA_STATUS(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<dim3(Hg, B), threads, smem, (cudaStream_t)stream>>>(
-      scores, count_sum, st, Hg, H_total, S_max, cap_max, cap_ratio, min_select, idx, n_out,
-      err_flag);
+      scores, count_sum, st, Hg, H_total, S_max, cap_max, cap_ratio, min_select, idx, n_out, err_flag, pos_prev,
+      slot_id, slot_used, frow, fslot, fcount, reinterpret_cast<unsigned long long*>(moved_rows));
   IG_LAUNCH_STATUS();
   return IG_OK;
+}
+}  // namespace ig
+
+extern "C" int ig_select(const float* scores, const int32_t* count_sum, const ig_step_state* st,
+                         int B, int Hg, int H_total, int S_max, int cap_max, double cap_ratio,
+                         int min_select, int32_t* idx, int32_t* n_out, int32_t* err_flag,
+                         void* stream) {
+  return ig::select_launch(scores, count_sum, st, B, Hg, H_total, S_max, cap_max, cap_ratio, min_select, idx, n_out,
+                           err_flag, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
+}
+
+extern "C" int ig_select_plan(const float* scores, const int32_t* count_sum, const ig_step_state* st, int B,
+                              int Hg, int H_total, int S_max, int cap_max, double cap_ratio, int min_select,
+                              int32_t* idx, int32_t* n_out, int32_t* err_flag, const int32_t* pos_prev,
+                              int32_t* slot_id, int32_t* slot_used, int32_t* frow, int32_t* fslot,
+                              int32_t* fcount, int64_t* moved_rows, void* stream) {
+  if (!slot_id) return IG_EINVAL;
+  return ig::select_launch(scores, count_sum, st, B, Hg, H_total, S_max, cap_max, cap_ratio, min_select, idx, n_out,
+                           err_flag, pos_prev, slot_id, slot_used, frow, fslot, fcount, moved_rows, stream);
 }
 
 extern "C" int ig_order_by_score(const float* scores, const int32_t* n, int B, int Hg, int S_max,

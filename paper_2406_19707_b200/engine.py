@@ -443,6 +443,9 @@ class DecodeEngine:
         # without record_selection / record_scores -- what the reference's run()
         # always keeps (one host sync per layer: a trace mode, not the perf path)
         self.record_trace = bool(record_trace)
+        # IG_FUSE_PLAN=1: the resident plan fused into the select (ig_select_plan) --
+        # measured 967 vs 989 tok/s at C3 (profiles/r02aa_*), so two launches by default
+        self.fuse_plan = os.environ.get("IG_FUSE_PLAN", "0") == "1"
         # IG_APPEND_FIRST=1: launch ig_append(li) before releasing the speculation
         # chain of li+1 (measured at C3: 952 vs 984 tok/s -- off)
         self.append_first = os.environ.get("IG_APPEND_FIRST", "0") == "1"
@@ -1423,16 +1426,28 @@ class DecodeEngine:
                         elif self.world > 1:
                             with torch.cuda.stream(SP):
                                 dist.all_reduce(self.count_sum[nxt], group=self.group)
-                        _lib.call("ig_select", self.scores.data_ptr(),
-                                  self.count_sum[nxt].data_ptr(), self.st.data_ptr(), B, Hg,
-                                  self.H, self.S_max, self.cap, float(sc.cap_ratio),
-                                  int(sc.min_select), self.idx[nxt].data_ptr(),
-                                  self.n[nxt].data_ptr(), self.err_ptr, sps)
+                        par = nxt % 2
+                        if resident and self.fuse_plan:
+                            # select + resident plan of each (b, h) in one CTA
+                            _lib.call("ig_select_plan", self.scores.data_ptr(),
+                                      self.count_sum[nxt].data_ptr(), self.st.data_ptr(), B, Hg,
+                                      self.H, self.S_max, self.cap, float(sc.cap_ratio),
+                                      int(sc.min_select), self.idx[nxt].data_ptr(),
+                                      self.n[nxt].data_ptr(), self.err_ptr, self.pos[nxt].data_ptr(),
+                                      self.slot_id[nxt - 1].data_ptr(),
+                                      self.slot_used[nxt - 1].data_ptr(), self.frow[par].data_ptr(),
+                                      self.fslot[par].data_ptr(), self.fcount[par].data_ptr(),
+                                      self.moved_rows[nxt].data_ptr(), sps)
+                        else:
+                            _lib.call("ig_select", self.scores.data_ptr(),
+                                      self.count_sum[nxt].data_ptr(), self.st.data_ptr(), B, Hg,
+                                      self.H, self.S_max, self.cap, float(sc.cap_ratio),
+                                      int(sc.min_select), self.idx[nxt].data_ptr(),
+                                      self.n[nxt].data_ptr(), self.err_ptr, sps)
                         self._mark("select", nxt, SP, False)
                         if cfg.record_scores:
                             spec_scores[nxt] = self.scores[:, :, :s].cpu()
-                        if resident:
-                            par = nxt % 2
+                        if resident and not self.fuse_plan:
                             _lib.call("ig_resident_plan", self.idx[nxt].data_ptr(),
                                       self.n[nxt].data_ptr(), self.pos[nxt].data_ptr(),
                                       self.slot_id[nxt - 1].data_ptr(),

@@ -348,3 +348,64 @@ def test_wide_batch_engine_matches_oracle(batch):
         _cmp_records(eng.records, ref_recs, ocfg.batch, exact=True)
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("S,cap,B,Hg", [(4100, 820, 3, 5), (600, 600, 2, 3), (33000, 6600, 1, 2)])
+def test_select_plan_fused_equals_two_launches(S, cap, B, Hg):
+    """ig_select_plan (the resident plan in the select's CTA) == ig_select
+    followed by ig_resident_plan: idx, n, slot tables, slot counts, fetch lists
+    and the moved-rows counter bit-identical, on random scores with ties,
+    partly filled slot tables with holes and a previous append position."""
+    import torch
+    from paper_2406_19707_b200 import _lib
+    g = torch.Generator(device="cuda")
+    g.manual_seed(S + cap)
+    s_len = S - 7
+    scores = torch.randint(-40, 40, (B, Hg, S), generator=g, device="cuda").float() / 8
+    count_sum = torch.randint(1, cap // 2, (B,), generator=g, device="cuda", dtype=torch.int32) * Hg
+    st = torch.zeros(8, dtype=torch.int32, device="cuda")
+    st[0] = s_len
+    slot0 = torch.full((B, Hg, cap), -1, dtype=torch.int32, device="cuda")
+    used0 = torch.randint(0, cap, (B, Hg), generator=g, device="cuda", dtype=torch.int32)
+    for b in range(B):
+        for h in range(Hg):
+            u = min(int(used0[b, h]), s_len)
+            used0[b, h] = u
+            rows = torch.randperm(s_len, generator=g, device="cuda")[:u].int()
+            rows[::5] = -1
+            slot0[b, h, :u] = rows
+    pos = torch.randint(0, s_len, (B, Hg), generator=g, device="cuda", dtype=torch.int32)
+    outs = []
+    for fused in (False, True):
+        idx = torch.full((B, Hg, cap), -7, dtype=torch.int32, device="cuda")
+        n = torch.zeros(B, dtype=torch.int32, device="cuda")
+        err = torch.zeros(1, dtype=torch.int32, device="cuda")
+        slot, used = slot0.clone(), used0.clone()
+        frow = torch.full((B, Hg, cap), -7, dtype=torch.int32, device="cuda")
+        fslot = torch.full((B, Hg, cap), -7, dtype=torch.int32, device="cuda")
+        fcount = torch.zeros((B, Hg), dtype=torch.int32, device="cuda")
+        moved = torch.zeros(1, dtype=torch.int64, device="cuda")
+        args = (scores.data_ptr(), count_sum.data_ptr(), st.data_ptr(), B, Hg, Hg, S, cap, 0.2, 1,
+                idx.data_ptr(), n.data_ptr(), err.data_ptr())
+        if fused:
+            _lib.call("ig_select_plan", *args, pos.data_ptr(), slot.data_ptr(), used.data_ptr(), frow.data_ptr(),
+                      fslot.data_ptr(), fcount.data_ptr(), moved.data_ptr(), _lib.stream_handle())
+        else:
+            _lib.call("ig_select", *args, _lib.stream_handle())
+            _lib.call("ig_resident_plan", idx.data_ptr(), n.data_ptr(), pos.data_ptr(), slot.data_ptr(),
+                      used.data_ptr(), B, Hg, cap, frow.data_ptr(), fslot.data_ptr(), fcount.data_ptr(),
+                      moved.data_ptr(), _lib.stream_handle())
+        torch.cuda.synchronize()
+        nn = n.cpu()
+        sel = [idx[b, :, :int(nn[b])].cpu() for b in range(B)]
+        fl = [(frow[b, h, :int(fcount[b, h])].cpu(), fslot[b, h, :int(fcount[b, h])].cpu())
+              for b in range(B) for h in range(Hg)]
+        outs.append((nn, sel, slot.cpu(), used.cpu(), fcount.cpu(), fl, moved.cpu(), err.cpu()))
+    a, b_ = outs
+    assert torch.equal(a[0], b_[0])
+    for x, y in zip(a[1], b_[1]):
+        assert torch.equal(x, y)
+    for k in (2, 3, 4, 6, 7):
+        assert torch.equal(a[k], b_[k]), k
+    for (r1, s1), (r2, s2) in zip(a[5], b_[5]):
+        assert torch.equal(r1, r2) and torch.equal(s1, s2)
