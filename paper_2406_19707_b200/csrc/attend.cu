@@ -1237,11 +1237,13 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
                   const ig_step_state* st, int Hg, int d, int cap, float sqrt_d, int max_chunks,
                   float* partial, int32_t* tickets, float* out, int ldo) {
   if constexpr (sizeof(T) == 2) {
-    // tcgen05 (attend_tc05.cu) only on request (IG_ATTEND_IMPL=c): it measured
-    // 6.07 vs 5.94 TB/s on 640 (b, h) x 4K-row sets but 73 vs 68 us at C3's 819-row
-    // sets and 105 vs 84 us at C4 (128 (b, h) x 6.5K rows), so the mma.sync
-    // kernels below stay the default (profiles/r02o_*, r02x_*).  -1 from the
-    // launcher: not applicable here.
+    // tcgen05 (attend_tc05.cu) only on request (IG_ATTEND_IMPL=c).  Alone it is the
+    // faster kernel on long row sets (640 x 4K rows: 6.42 vs 5.98 TB/s; C4's
+    // 128 x 6.5K: 82 vs 89 us) and the slower one on C3's 819-row sets (72 vs 62 us);
+    // inside the step its one CTA per SM with a 192-KB ring holds the SMs the
+    // speculation stream needs, so both C3 (962 vs 987 tok/s) and C4 (324 vs 329)
+    // run faster with the mma.sync kernels below (profiles/r02ae*, r02af*).
+    // -1 from the launcher: not applicable here.
     if (d == 128 && attend_impl() == 'c') {
       const int rc = attend_tc05_launch(std::is_same<T, __half>::value ? IG_ELT_F16 : IG_ELT_BF16, s, q, ldq, k_cur,
                                         v_cur, ldkv, stage, idx, n, rows_bh, pos, st, (int)grid.z, Hg, cap, sqrt_d,

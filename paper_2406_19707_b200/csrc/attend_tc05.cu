@@ -295,6 +295,7 @@ attend_tc05_kernel(const __grid_constant__ CUtensorMap tm, const float* __restri
 #pragma unroll
         for (int bx = 0; bx < 4; ++bx) tc05::tma_load_2d(dst + bx * kBox, &tm, bx * 64, row, &full[stage]);
       }
+      a5_mark_cta(3);
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
@@ -369,6 +370,7 @@ attend_tc05_kernel(const __grid_constant__ CUtensorMap tm, const float* __restri
       }
       if (!did) __nanosleep(20);
     }
+    if (lane == 0) a5_mark_cta(4);
   } else if (warp == 10) {
     // ---------------------------------------------------------------- q warp
     // per item: its q row -> power-of-two scaled exact split operand tile;
@@ -435,6 +437,7 @@ attend_tc05_kernel(const __grid_constant__ CUtensorMap tm, const float* __restri
       __syncwarp();
       tc05::mbar_arrive(&mfull[slot]);
     }
+    if (lane == 0) a5_mark_cta(5);
   } else {
     // ---------------------------------------------------------------- softmax (warps 2-5) / readout (6-9)
     const int q4 = warp & 3;
@@ -559,15 +562,29 @@ attend_tc05_kernel(const __grid_constant__ CUtensorMap tm, const float* __restri
         Lf = L * w;
         Of = acc * w;
       } else {
-        for (int t = 0; t < tiles_bh; ++t)
-          if (sc.item_start(x.bh, t)) Mf = fmaxf(Mf, __ldcg(pbase + (size_t)t * (d + 2)));
-        for (int t = 0; t < tiles_bh; ++t)
-          if (sc.item_start(x.bh, t)) {
-            const float mi = __ldcg(pbase + (size_t)t * (d + 2));
-            const float w = mi == -INFINITY ? 0.f : expf(mi - Mf);
-            Lf += __ldcg(pbase + (size_t)t * (d + 2) + 1) * w;
-            Of += __ldcg(pbase + (size_t)t * (d + 2) + 2 + r) * w;
+        // the (b, h)'s items start at tile 0 and at every CTA range start inside
+        // it: walk the ranges (a handful of 64-bit divisions, not one per tile --
+        // that walk cost ~30 us at C4's 52-tile row sets)
+        const long long g0 = prefix[x.bh], g1 = prefix[x.bh + 1];
+        const long long c0 = (g0 * sc.G + sc.TT - 1) / sc.TT;     // first range start >= g0
+        for (int pass = 0; pass < 2; ++pass) {
+          long long prev = -1;
+          for (long long c = c0 - 1; c < sc.G; ++c) {
+            const long long gs = c < c0 ? g0 : c * sc.TT / sc.G;  // item start (global tile)
+            if (gs == prev) continue;        // tile 0 again, or empty ranges (grid > tiles)
+            if (gs >= g1) break;
+            prev = gs;
+            const float* ps = pbase + (size_t)(gs - g0) * (d + 2);
+            if (pass == 0) {
+              Mf = fmaxf(Mf, __ldcg(ps));
+            } else {
+              const float mi = __ldcg(ps);
+              const float w = mi == -INFINITY ? 0.f : expf(mi - Mf);
+              Lf += __ldcg(ps + 1) * w;
+              Of += __ldcg(ps + 2 + r) * w;
+            }
           }
+        }
         if (r == 0) tickets[x.bh] = 0;
       }
       const float wc = expf(scur - Mf);
@@ -576,8 +593,10 @@ attend_tc05_kernel(const __grid_constant__ CUtensorMap tm, const float* __restri
     A5Tile x;
     if (warp < 6) {                    // softmax warps
       while (sc.next(x)) softmax(x);
+      if (r == 0) a5_mark_cta(6);
     } else {                           // readout warps
       while (sc.next(x)) readout(x);
+      if (r == 0) a5_mark_cta(7);
     }
   }
   __syncthreads();

@@ -75,6 +75,9 @@ def main():
     res["cta_end_us"] = [float((tr[:, 2].min() - t0) / 1e3), float((tr[:, 2].max() - t0) / 1e3)]
     ends = (tr[:, 2] - t0) / 1e3
     res["cta_end_by_block"] = [round(float(v), 1) for v in ends]
+    roles = ["producer", "mma", "qwarp", "softmax", "readout"]
+    res["role_end_by_block"] = {nm: [round(float((tr[c, 3 + i] - t0) / 1e3), 1) for c in range(G)]
+                                for i, nm in enumerate(roles)}
     names = ["load_issue", "s_issue", "pv_issue", "softmax_start", "softmax_end", "readout_end"]
     # per tile latencies, median over CTAs and tiles 1..n-2
     for i in range(1, 6):
