@@ -190,401 +190,12 @@ attend_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_
   if (threadIdx.x == 0) tickets[bh] = 0;
 }
 
-// Fast path for 512-B rows (d = 128, 2-byte elements): one 16-B vector per
-// lane moves a whole K+V row per warp instruction -- lanes 0-15 hold 8 K
-// elements each, lanes 16-31 hold 8 V elements; the q.k partials reduce over
-// the 16 K lanes and the score is broadcast.  kFastRows rows are in flight per
-// warp.  Same online softmax, same chunk / ticket merge as attend_kernel.
-constexpr int kFastRows = 8;
-constexpr int kFastChunk = 256;
-
-template <typename T>
-__device__ __forceinline__ void unpack8(const uint4& u, float* f) {
-  const T* h = reinterpret_cast<const T*>(&u);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) f[i] = Elt<T>::to_f(h[i]);
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kAttThreads)
-attend512_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_cur,
-                 const float* __restrict__ v_cur, int ldkv, const T* __restrict__ stage,
-                 const int32_t* __restrict__ idx, const int32_t* __restrict__ n_in,
-                 const int32_t* __restrict__ rows_bh, const int32_t* __restrict__ pos_in, const ig_step_state* __restrict__ st, int Hg,
-                 int cap, float sqrt_d, int max_chunks, float* __restrict__ partial,
-                 int32_t* __restrict__ tickets, float* __restrict__ out, int ldo) {
-  constexpr int d = 128;
-  const int b = blockIdx.z, h = blockIdx.y, c = blockIdx.x;
-  const size_t bh = (size_t)b * Hg + h;
-  const int rows = att_rows(rows_bh, n_in, st, b, bh);
-  const int nchunks = max(1, (rows + kFastChunk - 1) / kFastChunk);
-  if (c >= nchunks) return;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const bool klane = lane < 16;
-  const int e0 = (lane & 15) * 8;       // first of my 8 elements (K or V)
-  const int pos = att_pos(pos_in, st, bh);
-
-  float qv[8];
-  {
-    const float* qr = q + (size_t)b * ldq + (size_t)h * d + e0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) qv[i] = klane ? qr[i] : 0.f;
-  }
-  float m = -INFINITY, l = 0.f, acc[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-
-  auto consume = [&](float dot, const float* vv) {
-    // dot: per-lane partial (K lanes) -> full q.k in every lane
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    const float sc = __shfl_sync(0xffffffffu, dot, 0) / sqrt_d;
-    const float mn = fmaxf(m, sc);
-    const float corr = expf(m - mn);
-    const float p = expf(sc - mn);
-    l = l * corr + p;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = fmaf(p, vv[i], acc[i] * corr);
-    m = mn;
-  };
-
-  const int r0 = c * kFastChunk, r1 = min(rows, r0 + kFastChunk);
-  const uint4* base = reinterpret_cast<const uint4*>(stage + bh * (size_t)cap * 2 * d);
-  // Rows go in groups of kFastRows per warp.  The next group's loads are in
-  // flight while the current group is folded into the softmax, and a group is
-  // folded at once: kFastRows independent dot products / shuffle reductions,
-  // one running-max update, one rescale of (l, acc).
-  auto load_group = [&](int rb, uint4* raw, int& rowid) {
-    rowid = 0;
-    if (idx && lane < kFastRows && rb + lane < r1) rowid = idx[bh * cap + rb + lane];
-#pragma unroll
-    for (int u = 0; u < kFastRows; ++u) {
-      if (rb + u < r1)
-        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                     : "=r"(raw[u].x), "=r"(raw[u].y), "=r"(raw[u].z), "=r"(raw[u].w)
-                     : "l"(base + (size_t)(rb + u) * 32 + lane));
-      else  // a p = 0 weight times stale register bits could be 0 * NaN
-        raw[u] = make_uint4(0u, 0u, 0u, 0u);
-    }
-  };
-  const int step = kAttWarps * kFastRows;
-  int rb = r0 + w * kFastRows;
-  uint4 raw[kFastRows], nxt[kFastRows];
-  int rowid = 0, nrowid = 0;
-  if (rb < r1) load_group(rb, raw, rowid);
-  for (; rb < r1; rb += step) {
-    if (rb + step < r1) load_group(rb + step, nxt, nrowid);
-    float dot[kFastRows];
-#pragma unroll
-    for (int u = 0; u < kFastRows; ++u) {
-      float f[8];
-      unpack8<T>(raw[u], f);
-      float a = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) a = fmaf(qv[i], f[i], a);
-      dot[u] = klane ? a : 0.f;
-    }
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
-#pragma unroll
-      for (int u = 0; u < kFastRows; ++u) dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], o);
-    }
-    float gm = -INFINITY;
-#pragma unroll
-    for (int u = 0; u < kFastRows; ++u) {
-      const int id = idx ? __shfl_sync(0xffffffffu, rowid, u) : rb + u;
-      const bool ok = rb + u < r1 && id >= 0 && id != pos;   // id < 0: empty slot
-      dot[u] = ok ? __shfl_sync(0xffffffffu, dot[u], 0) / sqrt_d : -INFINITY;
-      if (!ok) raw[u] = make_uint4(0u, 0u, 0u, 0u);   // p = 0 must not meet stale bits
-      gm = fmaxf(gm, dot[u]);
-    }
-    if (gm != -INFINITY) {        // warp-uniform
-      const float mn = fmaxf(m, gm);
-      const float corr = expf(m - mn);
-      float psum = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] *= corr;
-#pragma unroll
-      for (int u = 0; u < kFastRows; ++u) {
-        const float p = expf(dot[u] - mn);   // exp(-inf) = 0 for skipped rows
-        psum += p;
-        float f[8];
-        unpack8<T>(raw[u], f);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = fmaf(p, f[i], acc[i]);
-      }
-      l = l * corr + psum;
-      m = mn;
-    }
-#pragma unroll
-    for (int u = 0; u < kFastRows; ++u) raw[u] = nxt[u];
-    rowid = nrowid;
-  }
-  if (c == 0 && w == 0) {  // the current token: GPU-resident f32 row
-    const float* src = (klane ? k_cur : v_cur) + (size_t)b * ldkv + (size_t)h * d + e0;
-    float f[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) f[i] = src[i];
-    float dot = 0.f;
-    if (klane) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) dot = fmaf(qv[i], f[i], dot);
-    }
-    consume(dot, f);
-  }
-
-  __shared__ float wm[kAttWarps], wl[kAttWarps];
-  __shared__ float wacc[kAttWarps][d];
-  if (lane == 0) { wm[w] = m; wl[w] = l; }
-  if (!klane) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) wacc[w][e0 + i] = acc[i];
-  }
-  __syncthreads();
-  float M = -INFINITY;
-  for (int i = 0; i < kAttWarps; ++i) M = fmaxf(M, wm[i]);
-  float* part = partial + (bh * max_chunks + c) * (size_t)(d + 2);
-  if (threadIdx.x == 0) {
-    float L = 0.f;
-    for (int i = 0; i < kAttWarps; ++i) L += wl[i] * (wm[i] == -INFINITY ? 0.f : expf(wm[i] - M));
-    part[0] = M;
-    part[1] = L;
-  }
-  for (int e = threadIdx.x; e < d; e += blockDim.x) {
-    float a = 0.f;
-    for (int i = 0; i < kAttWarps; ++i) a += wacc[i][e] * (wm[i] == -INFINITY ? 0.f : expf(wm[i] - M));
-    part[2 + e] = a;
-  }
-  __shared__ int last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(tickets + bh, 1) == nchunks - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  const float* pb = partial + bh * max_chunks * (size_t)(d + 2);
-  float MM = -INFINITY;
-  for (int i = 0; i < nchunks; ++i) MM = fmaxf(MM, __ldcg(pb + (size_t)i * (d + 2)));
-  float LL = 0.f;
-  for (int i = 0; i < nchunks; ++i) {
-    const float mi = __ldcg(pb + (size_t)i * (d + 2));
-    LL += __ldcg(pb + (size_t)i * (d + 2) + 1) * (mi == -INFINITY ? 0.f : expf(mi - MM));
-  }
-  for (int e = threadIdx.x; e < d; e += blockDim.x) {
-    float a = 0.f;
-    for (int i = 0; i < nchunks; ++i) {
-      const float mi = __ldcg(pb + (size_t)i * (d + 2));
-      a += __ldcg(pb + (size_t)i * (d + 2) + 2 + e) * (mi == -INFINITY ? 0.f : expf(mi - MM));
-    }
-    out[(size_t)b * ldo + (size_t)h * d + e] = a / LL;
-  }
-  if (threadIdx.x == 0) tickets[bh] = 0;
-}
-
-// TMA-fed variant of the 512-B-row path: the rows of a (b, h) chunk are
-// contiguous in the stage buffer, so thread 0 streams them into a 4-stage
-// shared-memory ring with one cp.async.bulk of up to 32 rows (16 KB) per stage
-// (mbarrier complete_tx); each warp folds 8 of a stage's rows into its online
-// softmax from shared memory.  Bytes in flight (48 KB per CTA) no longer cost
-// registers, which bounded the register-fed loop at ~0.44 of HBM.
-constexpr int kTmaRows = 32;      // rows per stage (one bulk copy)
-constexpr int kTmaStages = 4;
-constexpr int kTmaChunk = 512;    // rows per CTA
-
-__device__ __forceinline__ void att_mbar_init(uint32_t bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
-}
-__device__ __forceinline__ void att_mbar_expect(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void att_mbar_wait(uint32_t bar, uint32_t phase) {
-  asm volatile(
-      "{\n .reg .pred p;\n W_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra W_%=;\n}" ::"r"(bar), "r"(phase) : "memory");
-}
-__device__ __forceinline__ void att_bulk(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kAttThreads)
-attend512_tma_kernel(const float* __restrict__ q, int ldq, const float* __restrict__ k_cur,
-                     const float* __restrict__ v_cur, int ldkv, const T* __restrict__ stage,
-                     const int32_t* __restrict__ idx, const int32_t* __restrict__ n_in,
-                     const int32_t* __restrict__ rows_bh, const int32_t* __restrict__ pos_in, const ig_step_state* __restrict__ st,
-                     int Hg, int cap, float sqrt_d, int max_chunks, float* __restrict__ partial,
-                     int32_t* __restrict__ tickets, float* __restrict__ out, int ldo) {
-  constexpr int d = 128;
-  extern __shared__ __align__(128) uint4 ring[];          // [kTmaStages][kTmaRows][32]
-  __shared__ __align__(8) unsigned long long bars[kTmaStages];
-  const int b = blockIdx.z, h = blockIdx.y, c = blockIdx.x;
-  const size_t bh = (size_t)b * Hg + h;
-  const int rows = att_rows(rows_bh, n_in, st, b, bh);
-  const int nchunks = max(1, (rows + kTmaChunk - 1) / kTmaChunk);
-  if (c >= nchunks) return;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const bool klane = lane < 16;
-  const int e0 = (lane & 15) * 8;
-  const int pos = att_pos(pos_in, st, bh);
-  const int r0 = c * kTmaChunk, r1 = min(rows, r0 + kTmaChunk);
-  const int nst = (r1 - r0 + kTmaRows - 1) / kTmaRows;   // stages of this chunk (may be 0)
-  const uint8_t* src = reinterpret_cast<const uint8_t*>(stage + bh * (size_t)cap * 2 * d);
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kTmaStages; ++i) att_mbar_init((uint32_t)__cvta_generic_to_shared(&bars[i]));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  auto issue = [&](int j) {       // thread 0: stage j of this chunk -> ring slot j % kTmaStages
-    const int rs = r0 + j * kTmaRows, cnt = min(kTmaRows, r1 - rs);
-    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&bars[j % kTmaStages]);
-    att_mbar_expect(bar, (uint32_t)cnt * 512u);
-    att_bulk((uint32_t)__cvta_generic_to_shared(ring + (size_t)(j % kTmaStages) * kTmaRows * 32),
-             src + (size_t)rs * 512, (uint32_t)cnt * 512u, bar);
-  };
-  if (threadIdx.x == 0)
-    for (int j = 0; j < min(nst, kTmaStages); ++j) issue(j);
-
-  float qv[8];
-  {
-    const float* qr = q + (size_t)b * ldq + (size_t)h * d + e0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) qv[i] = klane ? qr[i] : 0.f;
-  }
-  float m = -INFINITY, l = 0.f, acc[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-
-  for (int j = 0; j < nst; ++j) {
-    const int rb = r0 + j * kTmaRows + w * 8;             // my 8 rows of this stage
-    int rowid = 0;
-    if (idx && lane < 8 && rb + lane < r1) rowid = idx[bh * cap + rb + lane];
-    att_mbar_wait((uint32_t)__cvta_generic_to_shared(&bars[j % kTmaStages]), (j / kTmaStages) & 1);
-    const uint4* sl = ring + (size_t)(j % kTmaStages) * kTmaRows * 32 + (size_t)(w * 8) * 32;
-    float dot[8];
-    uint4 raw[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      raw[u] = rb + u < r1 ? sl[u * 32 + lane] : make_uint4(0u, 0u, 0u, 0u);
-      float f[8];
-      unpack8<T>(raw[u], f);
-      float a = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) a = fmaf(qv[i], f[i], a);
-      dot[u] = klane ? a : 0.f;
-    }
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
-#pragma unroll
-      for (int u = 0; u < 8; ++u) dot[u] += __shfl_xor_sync(0xffffffffu, dot[u], o);
-    }
-    float gm = -INFINITY;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int id = idx ? __shfl_sync(0xffffffffu, rowid, u) : rb + u;
-      const bool ok = rb + u < r1 && id >= 0 && id != pos;   // id < 0: empty slot
-      dot[u] = ok ? __shfl_sync(0xffffffffu, dot[u], 0) / sqrt_d : -INFINITY;
-      if (!ok) raw[u] = make_uint4(0u, 0u, 0u, 0u);   // p = 0 must not meet stale bits
-      gm = fmaxf(gm, dot[u]);
-    }
-    if (gm != -INFINITY) {
-      const float mn = fmaxf(m, gm);
-      const float corr = expf(m - mn);
-      float psum = 0.f;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] *= corr;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const float p = expf(dot[u] - mn);
-        psum += p;
-        float f[8];
-        unpack8<T>(raw[u], f);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = fmaf(p, f[i], acc[i]);
-      }
-      l = l * corr + psum;
-      m = mn;
-    }
-    __syncthreads();                                        // ring slot j % S fully read
-    if (threadIdx.x == 0 && j + kTmaStages < nst) issue(j + kTmaStages);
-  }
-  if (c == 0 && w == 0) {  // the current token: GPU-resident f32 row
-    const float* srcr = (klane ? k_cur : v_cur) + (size_t)b * ldkv + (size_t)h * d + e0;
-    float f[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) f[i] = srcr[i];
-    float dot = 0.f;
-    if (klane) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) dot = fmaf(qv[i], f[i], dot);
-    }
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    const float sc = __shfl_sync(0xffffffffu, dot, 0) / sqrt_d;
-    const float mn = fmaxf(m, sc);
-    const float corr = expf(m - mn);
-    const float p = expf(sc - mn);
-    l = l * corr + p;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = fmaf(p, f[i], acc[i] * corr);
-    m = mn;
-  }
-
-  __shared__ float wm[kAttWarps], wl[kAttWarps];
-  __shared__ float wacc[kAttWarps][d];
-  if (lane == 0) { wm[w] = m; wl[w] = l; }
-  if (!klane) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) wacc[w][e0 + i] = acc[i];
-  }
-  __syncthreads();
-  float M = -INFINITY;
-  for (int i = 0; i < kAttWarps; ++i) M = fmaxf(M, wm[i]);
-  float* part = partial + (bh * max_chunks + c) * (size_t)(d + 2);
-  if (threadIdx.x == 0) {
-    float L = 0.f;
-    for (int i = 0; i < kAttWarps; ++i) L += wl[i] * (wm[i] == -INFINITY ? 0.f : expf(wm[i] - M));
-    part[0] = M;
-    part[1] = L;
-  }
-  for (int e = threadIdx.x; e < d; e += blockDim.x) {
-    float a = 0.f;
-    for (int i = 0; i < kAttWarps; ++i) a += wacc[i][e] * (wm[i] == -INFINITY ? 0.f : expf(wm[i] - M));
-    part[2 + e] = a;
-  }
-  __shared__ int last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(tickets + bh, 1) == nchunks - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  const float* pb = partial + bh * max_chunks * (size_t)(d + 2);
-  float MM = -INFINITY;
-  for (int i = 0; i < nchunks; ++i) MM = fmaxf(MM, __ldcg(pb + (size_t)i * (d + 2)));
-  float LL = 0.f;
-  for (int i = 0; i < nchunks; ++i) {
-    const float mi = __ldcg(pb + (size_t)i * (d + 2));
-    LL += __ldcg(pb + (size_t)i * (d + 2) + 1) * (mi == -INFINITY ? 0.f : expf(mi - MM));
-  }
-  for (int e = threadIdx.x; e < d; e += blockDim.x) {
-    float a = 0.f;
-    for (int i = 0; i < nchunks; ++i) {
-      const float mi = __ldcg(pb + (size_t)i * (d + 2));
-      a += __ldcg(pb + (size_t)i * (d + 2) + 2 + e) * (mi == -INFINITY ? 0.f : expf(mi - MM));
-    }
-    out[(size_t)b * ldo + (size_t)h * d + e] = a / LL;
-  }
-  if (threadIdx.x == 0) tickets[bh] = 0;
-}
-
 // ---------------------------------------------------------------------------
 // Tensor-core 512-B-row path (default for d = 128 with a 2-byte pool).
-// The per-row CUDA-core work of attend512_kernel (f16 -> f32 unpack, 16
-// FMAs and 5 shuffles per row and lane) bounded it at ~0.44 of HBM; here both
-// products run on mma.sync m16n8k16 over 16-row tiles:
+// Per-row CUDA-core work (f16 -> f32 unpack, 16 FMAs and 5 shuffles per row
+// and lane) bounded a register-fed version at ~0.44 of HBM and a TMA-fed one at
+// 0.37 (round 1; removed); here both products run on mma.sync m16n8k16 over
+// 16-row tiles:
 //   scores  S[16 rows x 8] = K_tile[16 x 128] . Qm[128 x 8], Qm's columns
 //           0..NS-1 = the f32 query split into NS parts exactly representable
 //           in T (q = q0 + q1 (+ q2)), so S[r][0] + .. + S[r][NS-1] is q.k to
@@ -598,7 +209,7 @@ attend512_tma_kernel(const float* __restrict__ q, int ldq, const float* __restri
 // ring by cp.async (16-B chunk c of row r stored at chunk c ^ (r & 7), so the
 // ldmatrix phases are conflict-free); a warp owns every 4th 16-row tile of
 // the CTA's chunk and keeps its own online softmax; warps and chunks merge in
-// fixed order as in attend512_kernel (deterministic).
+// fixed order (deterministic).
 // ---------------------------------------------------------------------------
 constexpr int kMmaWarps = 4;
 constexpr int kMmaTPW = 8;                                  // tiles per warp (default)
@@ -1211,15 +822,11 @@ attend512_wp_kernel(const float* __restrict__ q, int ldq, const float* __restric
   asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
-// IG_ATTEND_IMPL=tma selects the TMA-fed 512-B path.  Measured alone at C3
-// (round 1): register-fed 2.84 TB/s vs TMA-fed 2.39 TB/s -- the per-row math
-// (f16 unpack + shuffle reductions), not the feed, bounds this kernel, so
-// the register-fed loop stays the default.
-// 'm' (default: mma.sync), 'c' (tcgen05, attend_tc05.cu), 'r' (register-fed), 't' (TMA-fed)
+// IG_ATTEND_IMPL: 'm' (default: mma.sync), 'c' (tcgen05, attend_tc05.cu)
 inline char attend_impl() {
   static const char impl = [] {
     const char* v = getenv("IG_ATTEND_IMPL");
-    return v && (v[0] == 'r' || v[0] == 't' || v[0] == 'c') ? v[0] : 'm';
+    return v && v[0] == 'c' ? 'c' : 'm';
   }();
   return impl;
 }
@@ -1228,7 +835,6 @@ int attend_tc05_launch(int elt, cudaStream_t s, const float* q, int ldq, const f
                        int ldkv, const void* stage, const int32_t* idx, const int32_t* n, const int32_t* rows_bh,
                        const int32_t* pos, const ig_step_state* st, int B, int Hg, int cap, float sqrt_d,
                        int max_chunks, float* partial, int32_t* tickets, float* out, int ldo);
-inline bool attend_tma_enabled() { return attend_impl() == 't'; }
 
 template <typename T>
 int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const float* k_cur,
@@ -1250,18 +856,7 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
                                         max_chunks, partial, tickets, out, ldo);
       if (rc >= 0) return rc;
     }
-    if (d == 128 && attend_tma_enabled()) {  // 512-B rows, TMA-fed (opt-in)
-      const int mc = (cap + kTmaChunk - 1) / kTmaChunk;
-      const size_t smem = (size_t)kTmaStages * kTmaRows * 512;
-      IG_CUDA_STATUS(cudaFuncSetAttribute(attend512_tma_kernel<T>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attend512_tma_kernel<T><<<dim3(mc, grid.y, grid.z), kAttThreads, smem, s>>>(
-          q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, Hg, cap, sqrt_d,
-          max_chunks, partial, tickets, out, ldo);
-      IG_LAUNCH_STATUS();
-      return IG_OK;
-    }
-    if (d == 128 && (attend_impl() == 'm' || attend_impl() == 'c')) {  // 512-B rows, mma.sync
+    if (d == 128) {  // 512-B rows, mma.sync
       // IG_ATT_VARIANT (tuning sweeps): 0 = CTA per chunk, ring 2 x 8 tiles/warp (3 CTAs/SM),
       // 1 = ring 2 x 4 tiles, 2 = ring 3 x 8 tiles (2 CTAs/SM), 3 = ring 2 x 16 tiles,
       // 4 = warp-persistent (attend512_wp_kernel)
@@ -1333,14 +928,6 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
         default: IG_ATT_MMA(2, 8); break;
       }
 #undef IG_ATT_MMA
-      IG_LAUNCH_STATUS();
-      return IG_OK;
-    }
-    if (d == 128) {  // 512-B rows, register-fed (IG_ATTEND_IMPL=r)
-      const int mc = (cap + kFastChunk - 1) / kFastChunk;
-      attend512_kernel<T><<<dim3(mc, grid.y, grid.z), kAttThreads, 0, s>>>(
-          q, ldq, k_cur, v_cur, ldkv, (const T*)stage, idx, n, rows_bh, pos, st, Hg, cap, sqrt_d,
-          max_chunks, partial, tickets, out, ldo);
       IG_LAUNCH_STATUS();
       return IG_OK;
     }

@@ -10,17 +10,22 @@ are in HOW, not WHAT:
   * the KV pool is one pinned host allocation T[L][B][Hg][S_max][2][d]
     (fp16 by default: the reference's 2-byte accounting, engine.py:63) and
     its metadata lives in HBM;
-  * two CUDA streams: the compute stream runs LN / rehearsal / selection /
-    QKV / append / attention / W_O / FFN; the fetch stream moves the rows
-    layer i needs from the host pool while layer i-1 computes (the overlap
-    the reference models analytically in costmodel.py:102-139);
-  * with tensor parallelism over heads, each rank owns H/G heads, their
-    pools and partial keys; per layer it all-reduces the B head-count sums
-    (n averages over ALL heads, speculation.py:154-158) and the W_O output.
+  * three CUDA streams: the compute stream runs LN / QKV (+ the next layer's
+    speculation query) / append / attention / W_O / FFN, the speculation
+    stream runs layer i+1's rehearse -> select -> resident plan while layer i
+    computes, the fetch stream moves the rows that entered a selection from
+    the host pool into the HBM slot tables (the overlap the reference models
+    analytically in costmodel.py:102-139); one step replays as a CUDA graph;
+  * with tensor parallelism over heads (and Megatron-style FFN columns), each
+    rank owns H/G heads, their pools and partial keys; per layer it all-reduces
+    the B head-count sums (n averages over ALL heads, speculation.py:154-158)
+    and the W_O / FFN-out outputs over peer memory.
 
-Hot ops are the library kernels (ig_rehearse_count, ig_select, ig_fetch,
-ig_fetch_all, ig_append, ig_attend, ig_layernorm); the dense projections
-are plain fp32 cuBLAS GEMMs with TF32 off.  No CPU fallback exists.
+Hot ops are the library kernels (ig_rehearse_count, ig_select,
+ig_resident_plan, ig_fetch_slots, ig_append, ig_attend_slots, ig_layernorm);
+the dense projections are ig_sgemm_packed over weights packed once (f16 hi/lo,
+f32-accurate tensor-core GEMMs), the prefill's on ig_gemm_tc05 (tcgen05).
+No CPU fallback exists.
 """
 
 from __future__ import annotations

@@ -361,9 +361,9 @@ def test_sgemm_packed_vs_float64(M, N, K, epilogue):
 
 @pytest.mark.parametrize("elt", ["f16", "bf16"])
 def test_attend_512b_row_variants_match(elt):
-    """The three 512-B-row attention kernels -- tensor cores (default), register-fed
-    (IG_ATTEND_IMPL=r), TMA-fed (IG_ATTEND_IMPL=tma) -- each in a subprocess (the
-    switch is read once per process), vs float64 attention over the same rows:
+    """The two 512-B-row attention kernels -- mma.sync (default) and tcgen05
+    (IG_ATTEND_IMPL=c) -- each in a subprocess (the switch is read once per
+    process), vs float64 attention over the same rows:
     ragged row counts, an excluded row (pos), resident slot tables with empty
     slots (ig_attend_slots)."""
     import os
@@ -398,7 +398,7 @@ def test_attend_512b_row_variants_match(elt):
         "np.savez(sys.argv[1], out=out.cpu().numpy(), out2=out2.cpu().numpy(), q=q.cpu().numpy(),"
         " stage=stage.float().cpu().numpy(), slot=slot.cpu().numpy(), used=used.cpu().numpy())\n")
     res = {}
-    for impl in ("c", "mma", "r", "tma"):       # c = tcgen05 (default)
+    for impl in ("c", "mma"):                   # tcgen05 (opt-in), mma.sync (default)
         f = os.path.join(tempfile.mkdtemp(), "o.npz")
         env = dict(os.environ, IG_ATTEND_IMPL=impl)
         r = subprocess.run([sys.executable, "-c", code, f, elt], env=env, capture_output=True, text=True,
