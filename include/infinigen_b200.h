@@ -326,6 +326,15 @@ int ig_gemm_tc05(const void* A_hl, const float* inv_sa, const void* B_hl, const 
                  int N, int K, int Kp, float* C, int ldc, const float* R, int ldr, int epilogue,
                  int max_ctas, void* stream);
 
+/* Prefill causal attention on tcgen05 (model.py:156-180 causal, as used by
+ * forward_block model.py:195-244 in DecodeSession._prefill engine.py:245-291):
+ * qkv [nb N][ldqkv] f32 rows of (q | k | v) over Hg heads of d (64 or 128);
+ * out [nb N][ldo] f32, head h at columns [h d, (h+1) d).  q, k, v and p are
+ * split exactly into f16 hi/lo pairs (work: ig_prefill_attention_scratch bytes). */
+int ig_prefill_attention_scratch(int nb, int N, int Hg, int d, size_t* bytes);
+int ig_prefill_attention(const float* qkv, int ldqkv, int nb, int N, int Hg, int d, void* work,
+                         float* out, int ldo, void* stream);
+
 /* ---- diagnostics --------------------------------------------------------
  * ig_debug_attend_trace: device buffer (u64, >= grid x (8 + 6 x 64)) that the
  * tcgen05 attention fills with %globaltimer stamps per role and tile

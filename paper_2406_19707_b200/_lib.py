@@ -77,6 +77,8 @@ _SIGS = {
     "ig_layernorm": [_P, _P, _P, _F, _I, _I, _P, _P],
     "ig_split_f16": [_P, _I, _I, _I, _I, _I, _P, _P, _P],
     "ig_debug_attend_trace": [_P],
+    "ig_prefill_attention_scratch": [_I, _I, _I, _I, ctypes.POINTER(_SZ)],
+    "ig_prefill_attention": [_P, _I, _I, _I, _I, _I, _P, _P, _I, _P],
     "ig_gemm_tc05": [_P, _P, _P, _P, _I, _I, _I, _I, _P, _I, _P, _I, _I, _I, _P],
 }
 EXPORTS = tuple(_SIGS) + ("ig_status_string",)

@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["rehearse.cu", "select.cu", "pool.cu", "attend.cu", "gemm.cu", "gemm_packed.cu", "misc.cu",
            "resident.cu", "collective.cu", "gemm_tc05.cu",
-           "attend_tc05.cu"]
+           "attend_tc05.cu", "prefill_attn.cu"]
 LIB = os.path.join(HERE, "libinfinigen_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -857,7 +857,8 @@ class DecodeEngine:
         Layer-outer and batched over the sequences: layer li's weights are
         split once into tcgen05 operands (dense="tc05", the default:
         csrc/gemm_tc05.cu, f32-level hi/lo split GEMMs with the ReLU and the
-        residual adds fused into their epilogues), every sequence runs through
+        residual adds fused into their epilogues; the causal attention of all
+        the group's sequences in one launch of csrc/prefill_attn.cu), every sequence runs through
         the layer in groups of at most `chunk_rows` prompt rows, and the K/V
         rows, partial columns and partial keys of layer li are written without a
         host synchronisation.  dense="torch": cuBLAS GEMMs instead, IEEE fp32, or
@@ -925,9 +926,18 @@ class DecodeEngine:
                     qkv = mm(x_a, ops["qkv"], rm["qkv"], "x").view(nb, N, 3, Hg, d)
                     del x_a
                     att = torch.empty((nb, N, Hg, d), dtype=torch.float32, device=self.device)
+                    tc_att = tc and d in (64, 128)
+                    if tc_att:           # causal attention of every sequence on tcgen05, one launch
+                        sz = ctypes.c_size_t()
+                        _lib.call("ig_prefill_attention_scratch", nb, N, Hg, d, ctypes.byref(sz), kernels=0)
+                        if "att_work" not in ws or ws["att_work"].numel() < sz.value:
+                            ws["att_work"] = torch.empty(sz.value, dtype=torch.uint8, device=self.device)
+                        _lib.call("ig_prefill_attention", qkv.data_ptr(), 3 * Hgd, nb, N, Hg, d,
+                                  ws["att_work"].data_ptr(), att.data_ptr(), Hgd, _lib.stream_handle())
                     for j in range(nb):
                         q, k, v = (qkv[j, :, i].transpose(0, 1).contiguous() for i in range(3))
-                        att[j] = causal_attention(q, k, v).transpose(0, 1)
+                        if not tc_att:
+                            att[j] = causal_attention(q, k, v).transpose(0, 1)
                         b = b0 + j
                         # pool rows (keep_tok: which prompt token survives in each row)
                         kvrows = torch.stack([k[:, keep], v[:, keep]], dim=2).to(T).contiguous()

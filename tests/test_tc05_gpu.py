@@ -93,3 +93,50 @@ def test_gemm_tc05_few_ctas():
     assert float(((first.double() - ref).abs() / mag).max()) < 3e-6
     for ctas in (1, 3, 7):
         assert torch.equal(tcgemm.gemm(A, B, max_ctas=ctas), first), ctas
+
+
+def _prefill_attention(qkv, nb, N, Hg, d):
+    import ctypes
+    import torch
+    from paper_2406_19707_b200 import _lib
+    sz = ctypes.c_size_t()
+    _lib.call("ig_prefill_attention_scratch", nb, N, Hg, d, ctypes.byref(sz), kernels=0)
+    work = torch.empty(sz.value, dtype=torch.uint8, device="cuda")
+    out = torch.full((nb * N, Hg * d), float("nan"), device="cuda")
+    _lib.call("ig_prefill_attention", qkv.data_ptr(), qkv.stride(0), nb, N, Hg, d, work.data_ptr(), out.data_ptr(),
+              out.stride(0), _lib.stream_handle())
+    return out
+
+
+@pytest.mark.parametrize("nb,N,Hg,d", [(2, 200, 2, 128), (1, 1, 1, 128), (3, 129, 3, 64), (1, 700, 2, 64),
+                                       (2, 1000, 1, 128)])
+def test_prefill_attention_tc05_vs_float64(nb, N, Hg, d):
+    """ig_prefill_attention (csrc/prefill_attn.cu: two-pass causal attention on
+    tcgen05 with exact f16 hi/lo splits) vs float64 causal softmax attention
+    (model.py:156-180, causal): ragged query / key tiles, a single token, d 64
+    and 128, several sequences and heads; deterministic."""
+    import torch
+    g = torch.Generator(device="cuda")
+    g.manual_seed(nb * 1000 + N + Hg + d)
+    qkv = torch.randn(nb * N, 3 * Hg * d, device="cuda", generator=g) * 2
+    out = _prefill_attention(qkv, nb, N, Hg, d)
+    again = _prefill_attention(qkv, nb, N, Hg, d)
+    assert torch.equal(out, again)
+    x = qkv.double().view(nb, N, 3, Hg, d)
+    q, k, v = (x[:, :, i].permute(0, 2, 1, 3) for i in range(3))          # nb, Hg, N, d
+    s = q @ k.transpose(-1, -2) / float(torch.tensor(d, dtype=torch.float32).sqrt())
+    mask = torch.ones(N, N, dtype=torch.bool, device="cuda").tril()
+    s = s.masked_fill(~mask, float("-inf"))
+    ref = torch.softmax(s, dim=-1) @ v                                      # nb, Hg, N, d
+    ref = ref.permute(0, 2, 1, 3).reshape(nb * N, Hg * d)
+    err = float((out.double() - ref).abs().max())
+    # IEEE-f32 attention on the same inputs (torch math path) as the yardstick
+    xf = qkv.view(nb, N, 3, Hg, d)
+    qf, kf, vf = (xf[:, :, i].permute(0, 2, 1, 3) for i in range(3))
+    sf = (qf @ kf.transpose(-1, -2)) / torch.tensor(d, dtype=torch.float32).sqrt()
+    sf = sf.masked_fill(~mask, float("-inf"))
+    f32 = (torch.softmax(sf, dim=-1) @ vf).permute(0, 2, 1, 3).reshape(nb * N, Hg * d)
+    f32_err = float((f32.double() - ref).abs().max())
+    print(f"prefill attention nb{nb} N{N} Hg{Hg} d{d}: tc05 {err:.3g}  f32 {f32_err:.3g}")
+    assert torch.isfinite(out).all()
+    assert err < max(4 * f32_err, 1e-6), (err, f32_err)
