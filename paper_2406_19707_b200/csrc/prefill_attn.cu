@@ -25,7 +25,7 @@ namespace ig {
 namespace pa {
 constexpr int BQ = 128, BK = 64;
 constexpr int kThreads = 192;
-constexpr uint32_t kTmemCols = 512;      // S [0, 64), O main [128, 128 + D), O cross [256, 256 + D)
+constexpr uint32_t kTmemCols = 512;      // S [0, 64) / [64, 128), O main [128, 128 + D), O cross [256, 256 + D)
 
 template <int D> struct Geo {
   static constexpr int kBoxes = D / 64;                         // 64-element (128-B) boxes per part
@@ -80,12 +80,12 @@ prefill_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
   uint64_t* qfull = bars;
   uint64_t* full = bars + 1;      // [2]
   uint64_t* empty = bars + 3;     // [2]
-  uint64_t* sfull = bars + 5;
-  uint64_t* sfree = bars + 6;
-  uint64_t* pfull = bars + 7;
-  uint64_t* pfree = bars + 8;
-  uint64_t* ofull = bars + 9;
-  uint32_t* tmem_sh = (uint32_t*)(bars + 10);
+  uint64_t* sfull = bars + 5;     // [2] score buffers
+  uint64_t* sfree = bars + 7;     // [2]
+  uint64_t* pfull = bars + 9;
+  uint64_t* pfree = bars + 10;
+  uint64_t* ofull = bars + 11;
+  uint32_t* tmem_sh = (uint32_t*)(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = (N + BQ - 1) / BQ;
@@ -105,8 +105,10 @@ prefill_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
       tc05::mbar_init(&full[s], 1);
       tc05::mbar_init(&empty[s], 1);
     }
-    tc05::mbar_init(sfull, 1);
-    tc05::mbar_init(sfree, 128);
+    for (int s2 = 0; s2 < 2; ++s2) {
+      tc05::mbar_init(&sfull[s2], 1);
+      tc05::mbar_init(&sfree[s2], 128);
+    }
     tc05::mbar_init(pfull, 128);
     tc05::mbar_init(pfree, 1);
     tc05::mbar_init(ofull, 1);
@@ -144,56 +146,63 @@ prefill_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
+    // tile sequence g = 0 .. 2T-1 (pass 0: g = t, pass 1: g = T + t); the score
+    // MMAs run one tile ahead of the output MMAs (two TMEM score buffers)
     constexpr uint32_t idS = tc05::idesc_f16_f32(BQ, BK, 0, 0);
     constexpr uint32_t idO = tc05::idesc_f16_f32(BQ, D, 0, 1);
     tc05::mbar_wait(qfull, 0);
     tc05::fence_after_sync();
     const uint32_t qa = tc05::smem_u32(qs);
     const uint32_t pa_ = tc05::smem_u32(ps);
-    int seq = 0, sc = 0;              // sc: S tiles issued (sfree phases)
-    for (int pass = 0; pass < 2; ++pass)
-      for (int t = 0; t < T; ++t, ++seq) {
-        const int stage = seq & 1;
-        tc05::mbar_wait(&full[stage], (seq >> 1) & 1);
-        if (sc > 0) tc05::mbar_wait(sfree, (sc - 1) & 1);     // softmax has read the previous S
-        tc05::fence_after_sync();
-        const uint32_t kb = tc05::smem_u32(ring + stage * G::kStage);
-        if (tc05::elect_one()) {
+    const int total = 2 * T;
+    auto scores = [&](int g) {
+      const int stage = g & 1, sb = g & 1;
+      tc05::mbar_wait(&full[stage], (g >> 1) & 1);
+      if (g >= 2) tc05::mbar_wait(&sfree[sb], ((g - 2) >> 1) & 1);   // buffer's previous scores read
+      tc05::fence_after_sync();
+      const uint32_t kb = tc05::smem_u32(ring + stage * G::kStage);
+      if (tc05::elect_one()) {
 #pragma unroll
-          for (int j = 0; j < D / 16; ++j) {
-            const uint32_t ko = (j & 3) * 32;
-            const uint32_t qh = qa + (j >> 2) * (BQ * 128) + ko, ql = qh + G::kQPart;
-            const uint32_t kh = kb + (j >> 2) * (BK * 128) + ko, kl = kh + G::kKPart;
-            tc05::mma_f16(tmem, tc05::desc_kmajor_sw128(qh), tc05::desc_kmajor_sw128(kh), idS, j > 0 ? 1u : 0u);
-            tc05::mma_f16(tmem, tc05::desc_kmajor_sw128(qh), tc05::desc_kmajor_sw128(kl), idS, 1u);
-            tc05::mma_f16(tmem, tc05::desc_kmajor_sw128(ql), tc05::desc_kmajor_sw128(kh), idS, 1u);
-          }
-          tc05::mma_commit(sfull);
-          if (pass == 0) tc05::mma_commit(&empty[stage]);
+        for (int j = 0; j < D / 16; ++j) {
+          const uint32_t ko = (j & 3) * 32;
+          const uint32_t qh = qa + (j >> 2) * (BQ * 128) + ko, ql = qh + G::kQPart;
+          const uint32_t kh = kb + (j >> 2) * (BK * 128) + ko, kl = kh + G::kKPart;
+          const uint32_t d_s = tmem + 64 * sb;
+          tc05::mma_f16(d_s, tc05::desc_kmajor_sw128(qh), tc05::desc_kmajor_sw128(kh), idS, j > 0 ? 1u : 0u);
+          tc05::mma_f16(d_s, tc05::desc_kmajor_sw128(qh), tc05::desc_kmajor_sw128(kl), idS, 1u);
+          tc05::mma_f16(d_s, tc05::desc_kmajor_sw128(ql), tc05::desc_kmajor_sw128(kh), idS, 1u);
         }
-        __syncwarp();
-        ++sc;
-        if (pass == 1) {
-          tc05::mbar_wait(pfull, t & 1);                          // p of this tile is in shared memory
-          tc05::fence_after_sync();
-          const uint32_t vb = kb + G::kKBytes;
-          if (tc05::elect_one()) {
-#pragma unroll
-            for (int j = 0; j < BK / 16; ++j) {
-              const uint32_t ph = pa_ + j * 32, pl = ph + G::kPPart;
-              const uint32_t vh = vb + j * 2048, vl = vh + G::kKPart;
-              const uint32_t acc = (t > 0 || j > 0) ? 1u : 0u;
-              tc05::mma_f16(tmem + 128, tc05::desc_kmajor_sw128(ph), tc05::desc_mnmajor_sw128(vh, BK * 128), idO, acc);
-              tc05::mma_f16(tmem + 256, tc05::desc_kmajor_sw128(ph), tc05::desc_mnmajor_sw128(vl, BK * 128), idO, acc);
-              tc05::mma_f16(tmem + 256, tc05::desc_kmajor_sw128(pl), tc05::desc_mnmajor_sw128(vh, BK * 128), idO, 1u);
-            }
-            tc05::mma_commit(&empty[stage]);
-            tc05::mma_commit(pfree);
-            if (t == T - 1) tc05::mma_commit(ofull);
-          }
-          __syncwarp();
-        }
+        tc05::mma_commit(&sfull[sb]);
+        if (g < T) tc05::mma_commit(&empty[stage]);            // pass 0: only K was needed
       }
+      __syncwarp();
+    };
+    auto outputs = [&](int g) {                                 // pass 1 tile t = g - T
+      const int t = g - T, stage = g & 1;
+      tc05::mbar_wait(pfull, t & 1);
+      tc05::fence_after_sync();
+      const uint32_t vb = tc05::smem_u32(ring + stage * G::kStage) + G::kKBytes;
+      if (tc05::elect_one()) {
+#pragma unroll
+        for (int j = 0; j < BK / 16; ++j) {
+          const uint32_t ph = pa_ + j * 32, pl = ph + G::kPPart;
+          const uint32_t vh = vb + j * 2048, vl = vh + G::kKPart;
+          const uint32_t acc = (t > 0 || j > 0) ? 1u : 0u;
+          tc05::mma_f16(tmem + 128, tc05::desc_kmajor_sw128(ph), tc05::desc_mnmajor_sw128(vh, BK * 128), idO, acc);
+          tc05::mma_f16(tmem + 256, tc05::desc_kmajor_sw128(ph), tc05::desc_mnmajor_sw128(vl, BK * 128), idO, acc);
+          tc05::mma_f16(tmem + 256, tc05::desc_kmajor_sw128(pl), tc05::desc_mnmajor_sw128(vh, BK * 128), idO, 1u);
+        }
+        tc05::mma_commit(&empty[stage]);
+        tc05::mma_commit(pfree);
+        if (t == T - 1) tc05::mma_commit(ofull);
+      }
+      __syncwarp();
+    };
+    scores(0);
+    for (int g = 0; g < total; ++g) {
+      if (g + 1 < total) scores(g + 1);
+      if (g >= T) outputs(g);
+    }
   } else {
     // ---------------------------------------------------------------- softmax / epilogue
     const int q4 = warp & 3;
@@ -204,13 +213,14 @@ prefill_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     int sc = 0;
     for (int pass = 0; pass < 2; ++pass)
       for (int t = 0; t < T; ++t) {
-        tc05::mbar_wait(sfull, sc & 1);
+        const int sb = sc & 1;
+        tc05::mbar_wait(&sfull[sb], (sc >> 1) & 1);
         tc05::fence_after_sync();
         float s[BK];
 #pragma unroll
         for (int c0 = 0; c0 < BK; c0 += 32) {
           uint32_t v[32];
-          tc05::tmem_ld32(lanebase + c0, v);
+          tc05::tmem_ld32(lanebase + 64 * sb + c0, v);
           tc05::tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -219,7 +229,7 @@ prefill_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
           }
         }
         tc05::fence_before_sync();
-        tc05::mbar_arrive(sfree);
+        tc05::mbar_arrive(&sfree[sb]);
         ++sc;
         if (pass == 0) {
 #pragma unroll
