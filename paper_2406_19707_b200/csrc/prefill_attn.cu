@@ -13,8 +13,9 @@
 // pass 2 recomputes S, writes p = exp(s - m) (split) as the A operand of the
 // output MMAs and accumulates l = sum p.  Warp roles as in attend_tc05.cu:
 // warp 0 TMA producer (2-D tensor maps, 128-B swizzle, 2-stage ring of K|V
-// tiles), warp 1 single-thread tcgen05.mma issuer, warps 2-5 softmax /
-// epilogue (TMEM lane = query row).  One CTA per (q block, head, sequence),
+// tiles), warp 1 single-thread tcgen05.mma issuer (score MMAs one tile ahead,
+// two TMEM score buffers), warps 2-9 softmax / epilogue (TMEM lane = query
+// row, two warps per row: one per half of the key tile / output columns).  One CTA per (q block, head, sequence),
 // heaviest (latest) q blocks first.
 #include <cuda.h>
 
@@ -24,7 +25,7 @@
 namespace ig {
 namespace pa {
 constexpr int BQ = 128, BK = 64;
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;           // producer, MMA, 8 softmax warps (2 per TMEM lane quarter)
 constexpr uint32_t kTmemCols = 512;      // S [0, 64) / [64, 128), O main [128, 128 + D), O cross [256, 256 + D)
 
 template <int D> struct Geo {
@@ -35,7 +36,7 @@ template <int D> struct Geo {
   static constexpr uint32_t kKBytes = 2 * kKPart;               // K hi | K lo
   static constexpr uint32_t kStage = 2 * kKBytes;               // K | V
   static constexpr uint32_t kPPart = BQ * BK * 2;               // 16 KB
-  static constexpr size_t kSmem = 1024 + kQBytes + 2 * kStage + 2 * kPPart + 256;
+  static constexpr size_t kSmem = 1024 + kQBytes + 2 * kStage + 2 * kPPart + 128 + 2 * BQ * 4;   // <= 227 KB
 };
 }  // namespace pa
 
@@ -86,6 +87,9 @@ prefill_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
   uint64_t* pfree = bars + 10;
   uint64_t* ofull = bars + 11;
   uint32_t* tmem_sh = (uint32_t*)(bars + 12);
+  // [2 halves][128 rows]: the row max after pass 1, then l at the end (the second
+  // use cannot overtake a read of the first: every tile between waits for both halves)
+  float* xch = (float*)(bars + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nqb = (N + BQ - 1) / BQ;
@@ -107,9 +111,9 @@ prefill_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     }
     for (int s2 = 0; s2 < 2; ++s2) {
       tc05::mbar_init(&sfull[s2], 1);
-      tc05::mbar_init(&sfree[s2], 128);
+      tc05::mbar_init(&sfree[s2], 256);
     }
-    tc05::mbar_init(pfull, 128);
+    tc05::mbar_init(pfull, 256);
     tc05::mbar_init(pfree, 1);
     tc05::mbar_init(ofull, 1);
     tc05::fence_barrier_init();
@@ -205,27 +209,35 @@ prefill_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     }
   } else {
     // ---------------------------------------------------------------- softmax / epilogue
-    const int q4 = warp & 3;
+    // warps 2-9: lane quarter q4 = warp % 4, column half (32 of the 64 keys of a
+    // tile, D / 2 output columns); the two halves of a row combine m once (after
+    // pass 1) and l once (at the end) through shared memory
+    const int q4 = warp & 3, half = (warp - 2) >> 2;
     const int r = q4 * 32 + lane;                // query row of the block (TMEM lane)
     const int qi = q0 + r;
     const uint32_t lanebase = tmem + ((uint32_t)(q4 * 32) << 16);
+    constexpr int HK = BK / 2;
     float m = -INFINITY, l = 0.f;
     int sc = 0;
-    for (int pass = 0; pass < 2; ++pass)
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 1) {                           // the row max over both halves
+        xch[half * 128 + r] = m;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        m = fmaxf(m, xch[(half ^ 1) * 128 + r]);
+      }
       for (int t = 0; t < T; ++t) {
         const int sb = sc & 1;
         tc05::mbar_wait(&sfull[sb], (sc >> 1) & 1);
         tc05::fence_after_sync();
-        float s[BK];
-#pragma unroll
-        for (int c0 = 0; c0 < BK; c0 += 32) {
+        float s[HK];
+        {
           uint32_t v[32];
-          tc05::tmem_ld32(lanebase + 64 * sb + c0, v);
+          tc05::tmem_ld32(lanebase + 64 * sb + half * HK, v);
           tc05::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int key = t * BK + c0 + j;
-            s[c0 + j] = (key <= qi && key < N) ? __uint_as_float(v[j]) / sqrt_d : -INFINITY;
+          for (int j = 0; j < HK; ++j) {
+            const int key = t * BK + half * HK + j;
+            s[j] = (key <= qi && key < N) ? __uint_as_float(v[j]) / sqrt_d : -INFINITY;
           }
         }
         tc05::fence_before_sync();
@@ -233,7 +245,7 @@ prefill_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         ++sc;
         if (pass == 0) {
 #pragma unroll
-          for (int j = 0; j < BK; ++j) m = fmaxf(m, s[j]);
+          for (int j = 0; j < HK; ++j) m = fmaxf(m, s[j]);
           continue;
         }
         if (t > 0) tc05::mbar_wait(pfree, (t - 1) & 1);        // the previous tile's output MMAs read P
@@ -241,12 +253,14 @@ prefill_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         uint8_t* prow_h = ps + (r >> 3) * 1024 + (r & 7) * 128;
         uint8_t* prow_l = prow_h + G::kPPart;
 #pragma unroll
-        for (int c = 0; c < BK / 8; ++c) {
+        for (int cc = 0; cc < HK / 8; ++cc) {
+          const int c = half * (HK / 8) + cc;
           uint32_t hw[4], lw[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const float p0 = s[c * 8 + 2 * u] == -INFINITY ? 0.f : expf(s[c * 8 + 2 * u] - m);
-            const float p1 = s[c * 8 + 2 * u + 1] == -INFINITY ? 0.f : expf(s[c * 8 + 2 * u + 1] - m);
+            const float s0 = s[cc * 8 + 2 * u], s1 = s[cc * 8 + 2 * u + 1];
+            const float p0 = s0 == -INFINITY ? 0.f : expf(s0 - m);
+            const float p1 = s1 == -INFINITY ? 0.f : expf(s1 - m);
             l += p0 + p1;
             const __half2 hh = __floats2half2_rn(p0, p1);
             const float2 hf = __half22float2(hh);
@@ -261,14 +275,18 @@ prefill_attn_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         tc05::fence_proxy_async_smem();
         tc05::mbar_arrive(pfull);
       }
-    // ---- output: (O main + O cross) / l
+    }
+    // ---- output: (O main + O cross) / l, l summed over both halves
+    xch[half * 128 + r] = l;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    l += xch[(half ^ 1) * 128 + r];
     tc05::mbar_wait(ofull, 0);
     tc05::fence_after_sync();
     const bool live = qi < N;
     float* orow = out + ((size_t)b * N + (live ? qi : 0)) * ldo + (size_t)h * D;
     const float inv = 1.f / l;
 #pragma unroll 1
-    for (int c0 = 0; c0 < D; c0 += 32) {
+    for (int c0 = half * (D / 2); c0 < (half + 1) * (D / 2); c0 += 32) {
       uint32_t vm[32], vc[32];
       tc05::tmem_ld32(lanebase + 128 + c0, vm);
       tc05::tmem_ld32(lanebase + 256 + c0, vc);
