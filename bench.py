@@ -58,7 +58,7 @@ def _args():
     ap.add_argument("--fetch-priority", type=int, default=0, help="CUDA stream priority (-1 = high)")
     ap.add_argument("--fetch-impl", default="tma", choices=["ldg", "tma"])
     ap.add_argument("--fetch-rows", type=int, default=16, help="TMA rows per warp batch")
-    ap.add_argument("--dense", default="packed", choices=["ig", "tc", "cublas", "packed"])
+    ap.add_argument("--dense", default="packed", choices=["cublas", "packed"])
     ap.add_argument("--no-cuda-graph", dest="cuda_graph", action="store_false",
                     help="launch every kernel eagerly instead of replaying a captured decode step")
     ap.add_argument("--no-resident", dest="resident", action="store_false",
@@ -220,8 +220,7 @@ def _config(a) -> dict:
             "fetch": (f"{a.fetch_impl} x {a.fetch_ctas} CTAs x {a.fetch_threads} threads"
                       + (f" x {a.fetch_rows} rows/batch" if a.fetch_impl == "tma" else "")),
             "parallelism": f"tp{a.gpus} (attention heads + FFN columns)" if a.gpus > 1 else "single GPU",
-            "dense": {"ig": "ig_sgemm_rows (f32 CUDA cores)", "tc": "ig_sgemm_tc (3xTF32 tensor cores)",
-                      "packed": "ig_sgemm_packed (packed f16 hi/lo weights, 2xf16-split tensor cores, stream-K)",
+            "dense": {"packed": "ig_sgemm_packed (packed f16 hi/lo weights, 2xf16-split tensor cores, stream-K)",
                       "cublas": "cuBLAS f32 (TF32 off)"}[a.dense],
             "cuda_graph": bool(a.cuda_graph), "resident": bool(a.resident),
             "l2": "inputs larger than L2 (partial K >= 1.6 GB streamed per layer set; host pool 54 GB)"}

@@ -230,29 +230,13 @@ int ig_memcpy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t
                 size_t height, void* stream);
 
 /* ---- dense projections of the decode step (engine.py:323-327, 360-364) ----
- * Y[M][N] = X[M][K] . W[K][N] in IEEE f32, M <= 32 (sequences), W row-major;
- * epilogue 0 = none, 1 = ReLU, 2 = Y = R + X.W (residual).  K split over
- * `ksplit` CTAs per 128-column tile (ig_sgemm_rows_ksplit suggests one);
- * workspace >= ceil(N/128) * ksplit * M * 128 floats; tickets >= ceil(N/128)
- * ints, zeroed once and left zeroed.  Deterministic (fixed reduction order). */
-int ig_sgemm_rows_ksplit(int M, int N, int K);
-int ig_sgemm_rows(const float* X, int ldx, const float* W, int ldw, float* Y, int ldy,
-                  const float* R, int ldr, int M, int N, int K, int ksplit, int epilogue,
-                  float* workspace, size_t workspace_floats, int32_t* tickets, void* stream);
-
-/* Same contract on the tensor cores: 3xTF32 split precision (x = x_hi + x_lo,
- * w = w_hi + w_lo, each part TF32-rounded; x.w = x_hi.w_hi + x_hi.w_lo +
- * x_lo.w_hi with f32 accumulation) -- f32-level accuracy, not bit-identical
- * to ig_sgemm_rows.  Same workspace / ticket / ksplit rules.               */
-int ig_sgemm_tc_ksplit(int M, int N, int K);
-int ig_sgemm_tc(const float* X, int ldx, const float* W, int ldw, float* Y, int ldy,
-                const float* R, int ldr, int M, int N, int K, int ksplit, int epilogue,
-                float* workspace, size_t workspace_floats, int32_t* tickets, void* stream);
-
-/* Same contract and 3xTF32 arithmetic over weights PACKED once at load time
- * (ig_sgemm_pack: 16-KB blocks of 32 rows x 128 columns in MMA-fragment
- * order, contiguous in (column tile, row block) order -- the whole GEMM is one
- * sequential stream).  Persistent stream-K grid (no ksplit argument):
+ * Y[M][N] = X[M][K] . W[K][N], M <= 32 (sequences); epilogue 0 = none,
+ * 1 = ReLU, 2 = Y = R + X.W (residual).  f32-level split precision on the
+ * tensor cores over weights PACKED once at load time (ig_sgemm_pack: 32-KB
+ * blocks in MMA-fragment order, f16 hi/lo pairs -- 11 + 11 significand bits;
+ * x split the same way in registers; x.w = hi.hi + (hi.lo + lo.hi) with f32
+ * accumulation), contiguous in (column tile, row block) order -- the whole GEMM
+ * is one sequential stream.  Persistent stream-K grid:
  * ig_sgemm_packed_sizes gives the packed buffer (floats), the workspace
  * (floats) and ticket (ints, zeroed once, left zeroed) sizes for (M, N, K).
  * X 16-B aligned, ldx and K multiples of 4.  Deterministic on a given device. */

@@ -55,10 +55,6 @@ _SIGS = {
     "ig_fetch_slots": [_P, _P, _P, _P, _I, _I, _I, _I, _I, _P, _P],
     "ig_stage_put": [_P, _P, _I, _P, _P, _I, _I, _I, _I, _I, _P],
     "ig_memcpy2d": [_P, _SZ, _P, _SZ, _SZ, _SZ, _P],
-    "ig_sgemm_rows_ksplit": [_I, _I, _I],
-    "ig_sgemm_rows": [_P, _I, _P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _I, _P, _SZ, _P, _P],
-    "ig_sgemm_tc_ksplit": [_I, _I, _I],
-    "ig_sgemm_tc": [_P, _I, _P, _I, _P, _I, _P, _I, _I, _I, _I, _I, _I, _P, _SZ, _P, _P],
     "ig_sgemm_packed_sizes": [_I, _I, _I, ctypes.POINTER(_SZ), ctypes.POINTER(_SZ),
                               ctypes.POINTER(_SZ)],
     "ig_sgemm_pack": [_P, _I, _I, _I, _P, _P],

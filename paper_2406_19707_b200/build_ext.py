@@ -9,7 +9,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["rehearse.cu", "select.cu", "pool.cu", "attend.cu", "gemm.cu", "gemm_packed.cu", "misc.cu",
+SOURCES = ["rehearse.cu", "select.cu", "pool.cu", "attend.cu", "gemm_packed.cu", "misc.cu",
            "resident.cu", "collective.cu", "gemm_tc05.cu",
            "attend_tc05.cu", "prefill_attn.cu"]
 LIB = os.path.join(HERE, "libinfinigen_b200.so")

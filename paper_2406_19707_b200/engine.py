@@ -95,7 +95,7 @@ def _enable_ieee_fp32():
 
 class _Weight:
     """One decode-step weight matrix [K, N] of this rank: its row-major f32 copy
-    (dense paths "ig" / "tc" / "cublas") or its ig_sgemm_packed blocks
+    (dense="cublas") or its ig_sgemm_packed blocks
     (dense="packed": the row-major copy is dropped once packed)."""
 
     def __init__(self, rm: torch.Tensor | None, packed: bool, device, *, _shape=None):
@@ -418,8 +418,8 @@ class DecodeEngine:
             raise ValueError("fetch_impl must be 'ldg' or 'tma'")
         self.fetch_impl = fetch_impl
         self.fetch_rows = fetch_rows
-        if dense not in ("ig", "tc", "cublas", "packed"):
-            raise ValueError("dense must be 'ig', 'tc', 'cublas' or 'packed'")
+        if dense not in ("cublas", "packed"):
+            raise ValueError("dense must be 'packed' or 'cublas'")
         self.dense = dense
         self.cuda_graph = cuda_graph
         if cuda_graph and (config.record_selection or config.record_scores):
@@ -625,15 +625,10 @@ class DecodeEngine:
                           for _ in range(2 if spec_ and not self.resident else 0)]
         if self.resident:
             self._alloc_resident()
-        # skinny-GEMM workspace: the largest ceil(N/128) * ksplit * B * 128 over the projections
+        # packed-GEMM stream-K workspace: the largest over the projections
         Fg = self.Fg
         shapes = [(4 * Hg * d, D), (3 * Hg * d, D), (Hg * d, D), (D, Hg * d), (Fg, D), (D, Fg)]   # (N, K)
-        ws = 0
-        self.gemm_ksplit = {}
-        for N_, K_ in shapes:
-            ksp = self._ksplit(B, N_, K_)
-            self.gemm_ksplit[(N_, K_)] = ksp
-            ws = max(ws, ((N_ + 127) // 128) * ksp * B * 128)
+        ws = 1
         if self.dense == "packed":
             ws = 0
             for N_, K_ in shapes:
@@ -1198,10 +1193,6 @@ class DecodeEngine:
         return out
 
     # ----------------------------------------------------------------- decode
-    def _ksplit(self, M, N, K) -> int:
-        lib = _lib.load()
-        return lib.ig_sgemm_tc_ksplit(M, N, K) if self.dense == "tc" else lib.ig_sgemm_rows_ksplit(M, N, K)
-
     def _packed_weight(self, W: "_Weight"):
         return W.packed
 
@@ -1227,21 +1218,11 @@ class DecodeEngine:
             if self._inst is not None:
                 self._mark("dense", -1, self.compute, False)
             return
-        if self.dense == "cublas":
-            res = torch.addmm(R, X, W.rm) if epilogue == 2 else torch.matmul(X, W.rm)
-            if epilogue == 1:
-                res.relu_()
-            Y.copy_(res)              # Y may be a strided view (qkv of the fused buffer)
-            return
-        ksp = self.gemm_ksplit.get((N, K)) or self._ksplit(M, N, K)
-        if self._inst is not None:
-            self._mark("dense", -1, self.compute, True, 4 * (K * N + M * K + M * N))
-        _lib.call("ig_sgemm_tc" if self.dense == "tc" else "ig_sgemm_rows", X.data_ptr(), X.stride(0), W.rm.data_ptr(), W.rm.stride(0),
-                  Y.data_ptr(), Y.stride(0), _lib.ptr(R), R.stride(0) if R is not None else 0,
-                  M, N, K, ksp, epilogue, self.gemm_ws.data_ptr(), self.gemm_ws.numel(),
-                  self.gemm_tickets.data_ptr(), cs)
-        if self._inst is not None:
-            self._mark("dense", -1, self.compute, False)
+        # dense="cublas": IEEE-f32 torch GEMMs on the row-major weights (A/B only)
+        res = torch.addmm(R, X, W.rm) if epilogue == 2 else torch.matmul(X, W.rm)
+        if epilogue == 1:
+            res.relu_()
+        Y.copy_(res)              # Y may be a strided view (qkv of the fused buffer)
 
     def _issue_full_fetch(self, li: int, s: int, stage: torch.Tensor) -> None:
         self._mark("fetch", li, self.fetch_stream, True)

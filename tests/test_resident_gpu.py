@@ -146,9 +146,9 @@ SPEC_RUNS = sorted(r for r in RUNS if RUNS[r]["scheme"] == "speculative")
 
 @pytest.mark.parametrize("rname", SPEC_RUNS)
 @pytest.mark.parametrize("mname", ["m64", "m256"])
-@pytest.mark.parametrize("dense", ["ig", "tc", "packed"])
+@pytest.mark.parametrize("dense", ["cublas", "packed"])
 def test_resident_engine_matches_oracle(mname, rname, dense):
-    """dense="tc": the projections on 3xTF32 tensor cores -- still every
+    """dense="packed" (2xf16-split tensor cores) and IEEE-f32 cuBLAS: every
     selection identical to the oracle's (f32-level x_a)."""
     from paper_2406_19707_b200 import DecodeEngine
     _, sk = models(mname)

@@ -26,7 +26,7 @@ def main():
         sessions = [O.Session(sk, ocfg, O.random_prompt(40, 256, b)) for b in range(2)]
         for pool in ("f16", "f32"):
             for resident in (True, False):
-                for dense in ("packed", "tc", "ig"):
+                for dense in ("packed", "cublas"):
                     cfg = G.RunConfig(scheme="speculative", prompt_len=40, gen_len=4, batch=2,
                                       pool_limit=limit)
                     eng = G.DecodeEngine.from_sessions(sk, cfg, copy.deepcopy(sessions), pool_dtype=pool,
