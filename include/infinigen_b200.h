@@ -82,11 +82,15 @@ int ig_rehearse(const float* qspec, int ldq, const int32_t* cols, const float* p
  * The rehearsal tiles max-reduce into maxkey[b,h] and take a ticket; the last
  * tile of each (b, h) row counts score > float32(double(max) - alpha) over the
  * row and adds it to count_sum[b] (zero that first).  maxkey and tickets are
- * [B][Hg] scratch that must start zeroed and are left zeroed.               */
+ * [B][Hg] scratch that must start zeroed and are left zeroed.  row_range
+ * (optional, u32 [B][Hg][2]): that pass also records the row's maximum and
+ * minimum score as order keys, which ig_select then takes instead of
+ * scanning the row for them.                                                */
 int ig_rehearse_count(const float* qspec, int ldq, const int32_t* cols, const float* pk,
                       const ig_step_state* st, int B, int Hg, int d, int k, int S_max,
                       float scale, double alpha, float* scores, uint32_t* maxkey,
-                      int32_t* tickets, int32_t* counts, int32_t* count_sum, void* stream);
+                      int32_t* tickets, int32_t* counts, int32_t* count_sum, uint32_t* row_range,
+                      void* stream);
 
 /* Row maxima (as order keys) of scores not produced by ig_rehearse (the
  * select_tokens shim, speculation.py:156).                                  */
@@ -104,11 +108,13 @@ int ig_count(const float* scores, const uint32_t* maxkey, const ig_step_state* s
  * n[b] = min(clamp(floor(count_sum[b]/H_total + 0.5), min_select, cap), s),
  * cap = max(floor(cap_ratio*s), min_select); idx[b,h,0:n] = the top-n rows of
  * score[b,h] (ties -> lower index), written in ASCENDING row order.
- * Fails with IG_EINVAL at run time if n would exceed cap_max (buffer size). */
+ * If n would exceed cap_max (the buffer size) it is clamped and *err_flag set
+ * to 1.  row_range (optional): the rows' (max, min) order keys as
+ * ig_rehearse_count records them; NULL: computed here.                      */
 int ig_select(const float* scores, const int32_t* count_sum, const ig_step_state* st,
               int B, int Hg, int H_total, int S_max, int cap_max, double cap_ratio,
               int min_select, int32_t* idx, int32_t* n_out, int32_t* err_flag,
-              void* stream);
+              const uint32_t* row_range, void* stream);
 
 /* Drop-in ordering: rewrite idx[b,h,0:n] in the reference's stable
  * descending-score order (linalg.py:184).  Used by the select_tokens shim,
@@ -116,8 +122,6 @@ int ig_select(const float* scores, const int32_t* count_sum, const ig_step_state
 int ig_order_by_score(const float* scores, const int32_t* n, int B, int Hg,
                       int S_max, int cap, int32_t* idx, void* stream);
 
-/* Generic top-k per row (ties -> lower index), ascending output.  Used for
- * build_partial's column choice (speculation.py:41-58).                   */
 /* ig_select + ig_resident_plan of the same (b, h) in one launch (the plan runs
  * in the select's CTA on the selection it just wrote): same arguments as the
  * two calls, same results. */
@@ -125,7 +129,10 @@ int ig_select_plan(const float* scores, const int32_t* count_sum, const ig_step_
                    int Hg, int H_total, int S_max, int cap_max, double cap_ratio, int min_select,
                    int32_t* idx, int32_t* n_out, int32_t* err_flag, const int32_t* pos_prev,
                    int32_t* slot_id, int32_t* slot_used, int32_t* frow, int32_t* fslot,
-                   int32_t* fcount, int64_t* moved_rows, void* stream);
+                   int32_t* fcount, int64_t* moved_rows, const uint32_t* row_range, void* stream);
+
+/* Generic top-k per row (ties -> lower index), ascending output.  Used for
+ * build_partial's column choice (speculation.py:41-58).                   */
 int ig_topk_rows(const float* values, int rows, int len, int k, int32_t* idx_out,
                  void* stream);
 

@@ -33,10 +33,10 @@ _SIGS = {
     "ig_host_free": [_P],
     "ig_host_numa_node": [_P, ctypes.POINTER(_I)],
     "ig_rehearse": [_P, _I, _P, _P, _P, _I, _I, _I, _I, _I, _F, _P, _P, _P],
-    "ig_rehearse_count": [_P, _I, _P, _P, _P, _I, _I, _I, _I, _I, _F, _D, _P, _P, _P, _P, _P, _P],
+    "ig_rehearse_count": [_P, _I, _P, _P, _P, _I, _I, _I, _I, _I, _F, _D, _P, _P, _P, _P, _P, _P, _P],
     "ig_count": [_P, _P, _P, _I, _I, _I, _D, _P, _P, _P],
-    "ig_select": [_P, _P, _P, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P],
-    "ig_select_plan": [_P, _P, _P, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+    "ig_select": [_P, _P, _P, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _P],
+    "ig_select_plan": [_P, _P, _P, _I, _I, _I, _I, _I, _D, _I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
     "ig_order_by_score": [_P, _P, _I, _I, _I, _I, _P, _P],
     "ig_topk_rows": [_P, _I, _I, _I, _P, _P],
     "ig_fetch": [_P, _P, _P, _I, _I, _I, _I, _I, _P, _I, _I, _P],

@@ -69,7 +69,7 @@ layernorm_kernel(const float* __restrict__ x, const float* __restrict__ g,
 
 }  // namespace ig
 
-extern "C" int ig_abi_version(void) { return 1; }
+extern "C" int ig_abi_version(void) { return 2; }
 
 extern "C" const char* ig_status_string(int status) {
   switch (status) {

@@ -133,7 +133,7 @@ rehearse_count_kernel(const float* __restrict__ qspec, int ldq, const int32_t* _
                       int d, int k, int S_max, float scale, double alpha,
                       float* __restrict__ scores, uint32_t* __restrict__ maxkey,
                       int32_t* __restrict__ tickets, int32_t* __restrict__ counts,
-                      int32_t* __restrict__ count_sum) {
+                      int32_t* __restrict__ count_sum, uint32_t* __restrict__ row_range) {
   const int b = blockIdx.z, h = blockIdx.y;
   const int s = st->s_len;
   const int t0 = blockIdx.x * kRehearseChunk;
@@ -142,6 +142,7 @@ rehearse_count_kernel(const float* __restrict__ qspec, int ldq, const int32_t* _
   __shared__ float qs[kMaxK];
   __shared__ uint32_t wmax[kRehearseThreads / kWarp];
   __shared__ int red[kRehearseThreads / kWarp];
+  __shared__ uint32_t wmin[kRehearseThreads / kWarp];
   __shared__ int last;
   const size_t bh = (size_t)b * Hg + h;
   for (int j = threadIdx.x; j < k; j += blockDim.x)
@@ -183,16 +184,35 @@ rehearse_count_kernel(const float* __restrict__ qspec, int ldq, const int32_t* _
   __syncthreads();
   if (!last) return;
   __threadfence();
-  const float thr = __double2float_rn((double)key_to_float(__ldcg(maxkey + bh)) - alpha);
+  const uint32_t rmax = __ldcg(maxkey + bh);
+  const float thr = __double2float_rn((double)key_to_float(rmax) - alpha);
   int c = 0;
+  uint32_t kmin = 0xffffffffu;       // the row minimum for ig_select (row_range)
   for (int i = threadIdx.x * 4; i < s; i += blockDim.x * 4) {
     const float4 v = __ldcg(reinterpret_cast<const float4*>(row + i));
     c += (v.x > thr) + (v.y > thr) + (v.z > thr) + (v.w > thr);
+    if (row_range != nullptr) {
+      kmin = min(kmin, order_key(v.x));
+      if (i + 1 < s) kmin = min(kmin, order_key(v.y));
+      if (i + 2 < s) kmin = min(kmin, order_key(v.z));
+      if (i + 3 < s) kmin = min(kmin, order_key(v.w));
+    }
   }
   c = block_sum(c, red);
+  if (row_range != nullptr) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = kmin;
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
     counts[bh] = c;
     atomicAdd(count_sum + b, c);     // integer: exact, order-free
+    if (row_range != nullptr) {      // the row's (max, min) order keys: ig_select skips its P0 pass
+      for (int i = 1; i < kRehearseThreads / kWarp; ++i) kmin = min(kmin, wmin[i]);
+      row_range[2 * bh] = rmax;
+      row_range[2 * bh + 1] = kmin;
+    }
     maxkey[bh] = 0;                  // scratch ready for the next launch
     tickets[bh] = 0;
   }
@@ -204,7 +224,7 @@ extern "C" int ig_rehearse_count(const float* qspec, int ldq, const int32_t* col
                                  const ig_step_state* st, int B, int Hg, int d, int k, int S_max,
                                  float scale, double alpha, float* scores, uint32_t* maxkey,
                                  int32_t* tickets, int32_t* counts, int32_t* count_sum,
-                                 void* stream) {
+                                 uint32_t* row_range, void* stream) {
   using namespace ig;
   if (B < 1 || Hg < 1 || d < 1 || k < 1 || k > d || k > kMaxK || S_max < 1 || (S_max & 3) ||
       ldq < Hg * d || !(alpha > 0) || !qspec || !cols || !pk || !st || !scores || !maxkey ||
@@ -213,7 +233,7 @@ extern "C" int ig_rehearse_count(const float* qspec, int ldq, const int32_t* col
   dim3 grid((S_max + kRehearseChunk - 1) / kRehearseChunk, Hg, B);
   rehearse_count_kernel<<<grid, kRehearseThreads, 0, (cudaStream_t)stream>>>(
       qspec, ldq, cols, pk, st, Hg, d, k, S_max, scale, alpha, scores, maxkey, tickets, counts,
-      count_sum);
+      count_sum, row_range);
   IG_LAUNCH_STATUS();
   return IG_OK;
 }

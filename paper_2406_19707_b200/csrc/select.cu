@@ -175,7 +175,7 @@ struct BinShared {
   int scan[kSelWarps];
   int warp_a[kSelWarps];      // rows of the warp's range surely taken
   int warp_b[kSelWarps];      // radix mode: rows of b* whose key == P
-  int bstar, need, m, ncand;
+  int bstar, need, m, ncand, nn;
   SelShared rx;               // radix fallback
 };
 
@@ -220,63 +220,79 @@ __device__ __forceinline__ int select_row(const float* __restrict__ scores, cons
                                           const ig_step_state* __restrict__ st, int Hg, int H_total, int S_max,
                                           int cap_max, double cap_ratio, int min_select, int32_t* __restrict__ idx,
                                           int32_t* __restrict__ n_out, int32_t* __restrict__ err_flag,
-                                          BinShared& sh, uint32_t* __restrict__ bits) {
+                                          const uint32_t* __restrict__ row_range, BinShared& sh,
+                                          uint32_t* __restrict__ bits) {
   constexpr int NW = THREADS / kWarp;
   constexpr int PER = kBins / THREADS;
   const int b = blockIdx.y, h = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int s = st->s_len;
-  // n = floor(sum/H + 0.5) == floor((2 sum + H) / 2H) exactly (integers)
-  const long long sum = count_sum[b];
-  long long n = (2 * sum + H_total) / (2LL * H_total);
-  const long long cap = max((long long)floor(cap_ratio * (double)s), (long long)min_select);
-  n = min(max(n, (long long)min_select), cap);
-  n = min(n, (long long)s);
-  int nn = (int)n;
-  if (nn > cap_max) {  // caller sized the index buffer too small: flag and clamp
-    // a plain store (the flag may live in mapped host memory, where device
-    // atomics are not guaranteed): only ever 0 -> 1
-    if (tid == 0) *reinterpret_cast<volatile int32_t*>(err_flag) = 1;
-    nn = cap_max;
-  }
-  if (h == 0 && tid == 0) n_out[b] = nn;
   const size_t bh = (size_t)b * Hg + h;
   const float* row = scores + bh * S_max;
   int32_t* out = idx + bh * cap_max;
+  if (tid == 0) {
+    // n = floor(sum/H + 0.5) == floor((2 sum + H) / 2H) exactly (integers)
+    const long long sum = count_sum[b];
+    long long n = (2 * sum + H_total) / (2LL * H_total);
+    const long long cap = max((long long)floor(cap_ratio * (double)s), (long long)min_select);
+    n = min(max(n, (long long)min_select), cap);
+    n = min(n, (long long)s);
+    int nn = (int)n;
+    if (nn > cap_max) {  // caller sized the index buffer too small: flag and clamp
+      // a plain store (the flag may live in mapped host memory, where device
+      // atomics are not guaranteed): only ever 0 -> 1
+      *reinterpret_cast<volatile int32_t*>(err_flag) = 1;
+      nn = cap_max;
+    }
+    if (h == 0) n_out[b] = nn;
+    sh.nn = nn;
+  }
+
+  // ---- P0: row min / max (order keys) -- from ig_rehearse_count's last-tile
+  // pass when it recorded them (row_range), else one pass over the row
+  uint32_t kmin = 0xffffffffu, kmax = 0u;
+  if (row_range != nullptr) {
+    kmax = __ldcg(row_range + 2 * bh);
+    kmin = __ldcg(row_range + 2 * bh + 1);
+  } else {
+    for (int t = tid * 4; t < s; t += THREADS * 4) {
+      const float4 v = row4(row, t);
+      const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (t + i < s) {
+          const uint32_t k = order_key(x[i]);
+          kmin = min(kmin, k);
+          kmax = max(kmax, k);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+      kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    }
+    if (lane == 0) { sh.kmin[w] = kmin; sh.kmax[w] = kmax; }
+  }
+  for (int i = tid; i < kBins; i += THREADS) sh.hist[i] = 0;
+  __syncthreads();
+  const int nn = sh.nn;
   if (nn >= s) {
     for (int t = tid; t < s; t += THREADS) out[t] = t;
     return s;
   }
   if (nn <= 0) return 0;
-
-  // ---- P0: row min / max (order keys)
-  uint32_t kmin = 0xffffffffu, kmax = 0u;
-  for (int t = tid * 4; t < s; t += THREADS * 4) {
-    const float4 v = row4(row, t);
-    const float x[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (t + i < s) {
-        const uint32_t k = order_key(x[i]);
-        kmin = min(kmin, k);
-        kmax = max(kmax, k);
-      }
+  if (row_range == nullptr) {
+    kmin = sh.kmin[0];
+    kmax = sh.kmax[0];
+    for (int i = 1; i < NW; ++i) { kmin = min(kmin, sh.kmin[i]); kmax = max(kmax, sh.kmax[i]); }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-  }
-  if (lane == 0) { sh.kmin[w] = kmin; sh.kmax[w] = kmax; }
-  for (int i = tid; i < kBins; i += THREADS) sh.hist[i] = 0;
-  __syncthreads();
-  kmin = sh.kmin[0];
-  kmax = sh.kmax[0];
-  for (int i = 1; i < NW; ++i) { kmin = min(kmin, sh.kmin[i]); kmax = max(kmax, sh.kmax[i]); }
   const float hi = key_to_float(kmax), lo = key_to_float(kmin);
   float scale = (float)kBins / (hi - lo);
   if (!(scale < 1e30f)) scale = 0.f;            // flat (or denormal-range) row: one bin
 
+  // warp w owns rows [t_lo, t_hi), a multiple of 128 (its float4 lanes)
+  const int span = ((s + NW - 1) / NW + 127) & ~127;
+  const int t_lo = min(s, w * span), t_hi = min(s, t_lo + span);
   // ---- P1: value-bin histogram, boundary bin
   for (int t = tid * 4; t < s; t += THREADS * 4) {
     const float4 v = row4(row, t);
@@ -313,9 +329,6 @@ __device__ __forceinline__ int select_row(const float* __restrict__ scores, cons
   // 0: the whole boundary bin is taken; 1: candidates ranked; 2: radix select in b*
   const int mode = (m == need) ? 0 : (m <= kCandMax ? 1 : 2);
 
-  // warp w owns rows [t_lo, t_hi), a multiple of 128 (its float4 lanes)
-  const int span = ((s + NW - 1) / NW + 127) & ~127;
-  const int t_lo = min(s, w * span), t_hi = min(s, t_lo + span);
 
   // ---- P2: per-warp counts (+ candidate gather / radix resolve of b*)
   uint32_t P = 0u;          // radix mode: the key of the need-th largest row in b*
@@ -405,6 +418,41 @@ __device__ __forceinline__ int select_row(const float* __restrict__ scores, cons
 
   // ---- P3: ascending emission
   int out_off = 0, eq_before = 0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  if (mode != 2) {
+    out_off = warp_sum(lane < w ? sh.warp_a[lane] : 0);      // rows of the warps before mine
+    // no tie cut inside b*: a row is taken iff its bin is < b*, or == b* and
+    // (whole bin, or its candidate bit is set).  Ranks from four ballots (one
+    // per float4 position): the rows before (lane, i) are every taken row of
+    // lanes < lane plus this lane's taken rows at positions < i.
+    for (int t0 = t_lo; t0 < t_hi; t0 += 128) {
+      const int t = t0 + lane * 4;
+      int bn[4] = {kBins, kBins, kBins, kBins};
+      if (t < t_hi) {
+        const float4 v = row4(row, t);
+        const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (t + i < t_hi) bn[i] = vbin(x[i], hi, scale);
+      }
+      bool take[4];
+      int before = 0, total = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        take[i] = bn[i] < bstar ||
+                  (bn[i] == bstar && (mode == 0 || ((bits[(t + i) >> 5] >> ((t + i) & 31)) & 1u)));
+        const unsigned mb = __ballot_sync(0xffffffffu, take[i]);
+        before += __popc(mb & lt_mask);
+        total += __popc(mb);
+      }
+      int pos = out_off + before;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (take[i]) out[pos++] = t + i;
+      out_off += total;
+    }
+    return nn;
+  }
   for (int i = 0; i < w; ++i) {
     const int ee = min(sh.warp_b[i], max(0, need_eq - eq_before));
     eq_before += sh.warp_b[i];
@@ -474,18 +522,18 @@ __device__ __forceinline__ int select_row(const float* __restrict__ scores, cons
 // of the same (b, h) runs in the same CTA on the selection just written --
 // one launch and one dependent hop fewer on the speculation chain)
 template <int THREADS, bool PLAN>
-__global__ void __launch_bounds__(THREADS)
+__global__ void __launch_bounds__(THREADS) __maxnreg__(THREADS == 1024 ? 64 : 32)   // 1024: no spills at C4 row lengths
 select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ count_sum,
               const ig_step_state* __restrict__ st, int Hg, int H_total, int S_max, int cap_max,
               double cap_ratio, int min_select, int32_t* __restrict__ idx,
               int32_t* __restrict__ n_out, int32_t* __restrict__ err_flag, const int32_t* __restrict__ pos_prev,
               int32_t* __restrict__ slot_id, int32_t* __restrict__ slot_used, int32_t* __restrict__ frow,
               int32_t* __restrict__ fslot, int32_t* __restrict__ fcount,
-              unsigned long long* __restrict__ moved_rows) {
+              unsigned long long* __restrict__ moved_rows, const uint32_t* __restrict__ row_range) {
   __shared__ BinShared sh;
   extern __shared__ uint32_t bits[];            // take bitmap, ceil(S_max / 32) words (+ plan scratch)
   const int n = select_row<THREADS>(scores, count_sum, st, Hg, H_total, S_max, cap_max, cap_ratio, min_select,
-                                    idx, n_out, err_flag, sh, bits);
+                                    idx, n_out, err_flag, row_range, sh, bits);
   if constexpr (PLAN) {
     const size_t bh = (size_t)blockIdx.y * Hg + blockIdx.x;
     int32_t* freelist = reinterpret_cast<int32_t*>(bits + (S_max + 31) / 32);
@@ -539,7 +587,7 @@ static int select_launch(const float* scores, const int32_t* count_sum, const ig
                          int H_total, int S_max, int cap_max, double cap_ratio, int min_select, int32_t* idx,
                          int32_t* n_out, int32_t* err_flag, const int32_t* pos_prev, int32_t* slot_id,
                          int32_t* slot_used, int32_t* frow, int32_t* fslot, int32_t* fcount, int64_t* moved_rows,
-                         void* stream) {
+                         const uint32_t* row_range, void* stream) {
   if (B < 1 || Hg < 1 || H_total < Hg || S_max < 1 || cap_max < 1 || !(cap_ratio > 0) ||
       cap_ratio > 1 || min_select < 1 || !scores || !count_sum || !st || !idx || !n_out ||
       !err_flag)
@@ -550,10 +598,11 @@ static int select_launch(const float* scores, const int32_t* count_sum, const ig
   // the take bitmap (+ the plan's free list and match flags)
   const size_t smem = (size_t)(S_max + 31) / 32 * 4 + (plan ? (size_t)cap_max * 5 : 0);
   if (smem > 200 * 1024) return IG_EINVAL;
-  // IG_SELECT_THREADS=256|512 for rows up to kSelLongRows (A/B: how many CTAs fit one wave)
+  // rows up to kSelLongRows: 256 threads (5 CTAs/SM: C3's 640 rows in one wave);
+  // IG_SELECT_THREADS=512 for the A/B
   static const int short_threads = [] {
     const char* e = getenv("IG_SELECT_THREADS");
-    return e && atoi(e) == 256 ? 256 : kSelThreads;
+    return e && atoi(e) == 512 ? kSelThreads : 256;
   }();
   const int threads = S_max > kSelLongRows ? kSelThreadsLong : short_threads;
   auto pick = [&](auto k512, auto k256, auto k1024) {
@@ -567,7 +616,7 @@ static int select_launch(const float* scores, const int32_t* count_sum, const ig
     IG_CUDA_STATUS(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<dim3(Hg, B), threads, smem, (cudaStream_t)stream>>>(
       scores, count_sum, st, Hg, H_total, S_max, cap_max, cap_ratio, min_select, idx, n_out, err_flag, pos_prev,
-      slot_id, slot_used, frow, fslot, fcount, reinterpret_cast<unsigned long long*>(moved_rows));
+      slot_id, slot_used, frow, fslot, fcount, reinterpret_cast<unsigned long long*>(moved_rows), row_range);
   IG_LAUNCH_STATUS();
   return IG_OK;
 }
@@ -576,19 +625,21 @@ static int select_launch(const float* scores, const int32_t* count_sum, const ig
 extern "C" int ig_select(const float* scores, const int32_t* count_sum, const ig_step_state* st,
                          int B, int Hg, int H_total, int S_max, int cap_max, double cap_ratio,
                          int min_select, int32_t* idx, int32_t* n_out, int32_t* err_flag,
-                         void* stream) {
+                         const uint32_t* row_range, void* stream) {
   return ig::select_launch(scores, count_sum, st, B, Hg, H_total, S_max, cap_max, cap_ratio, min_select, idx, n_out,
-                           err_flag, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
+                           err_flag, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, row_range,
+                           stream);
 }
 
 extern "C" int ig_select_plan(const float* scores, const int32_t* count_sum, const ig_step_state* st, int B,
                               int Hg, int H_total, int S_max, int cap_max, double cap_ratio, int min_select,
                               int32_t* idx, int32_t* n_out, int32_t* err_flag, const int32_t* pos_prev,
                               int32_t* slot_id, int32_t* slot_used, int32_t* frow, int32_t* fslot,
-                              int32_t* fcount, int64_t* moved_rows, void* stream) {
+                              int32_t* fcount, int64_t* moved_rows, const uint32_t* row_range, void* stream) {
   if (!slot_id) return IG_EINVAL;
   return ig::select_launch(scores, count_sum, st, B, Hg, H_total, S_max, cap_max, cap_ratio, min_select, idx, n_out,
-                           err_flag, pos_prev, slot_id, slot_used, frow, fslot, fcount, moved_rows, stream);
+                           err_flag, pos_prev, slot_id, slot_used, frow, fslot, fcount, moved_rows, row_range,
+                           stream);
 }
 
 extern "C" int ig_order_by_score(const float* scores, const int32_t* n, int B, int Hg, int S_max,

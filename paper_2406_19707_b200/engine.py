@@ -606,6 +606,9 @@ class DecodeEngine:
         self.hidden = torch.empty((B, self.Fg), dtype=f32, device=dev)
         self.scores = torch.empty((B, Hg, S), dtype=f32, device=dev)
         self.maxkey = torch.zeros((B, Hg), dtype=i32, device=dev)      # rehearse scratch
+        # each row's (max, min) score order keys, written by ig_rehearse_count's
+        # last-tile pass and read by ig_select (no min/max pass of its own)
+        self.row_range = torch.zeros((B, Hg, 2), dtype=i32, device=dev)
         self.rtickets = torch.zeros((B, Hg), dtype=i32, device=dev)    # (left zeroed)
         self.counts = torch.zeros((B, Hg), dtype=i32, device=dev)
         self.count_sum = torch.zeros((L, B), dtype=i32, device=dev)
@@ -1090,7 +1093,7 @@ class DecodeEngine:
                       self.pk[li - 1].data_ptr(), self.st.data_ptr(), B, Hg, d, kc, S, self.scale,
                       float(sc.alpha), self.scores.data_ptr(), self.maxkey.data_ptr(),
                       self.rtickets.data_ptr(), self.counts.data_ptr(),
-                      self.count_sum[li].data_ptr(), h)
+                      self.count_sum[li].data_ptr(), self.row_range.data_ptr(), h)
 
         idx_tmp = torch.empty_like(self.idx[li])
         n_tmp = torch.empty_like(self.n[li])
@@ -1098,7 +1101,8 @@ class DecodeEngine:
         def select():
             _lib.call("ig_select", self.scores.data_ptr(), self.count_sum[li].data_ptr(),
                       self.st.data_ptr(), B, Hg, self.H, S, self.cap, float(sc.cap_ratio),
-                      int(sc.min_select), idx_tmp.data_ptr(), n_tmp.data_ptr(), self.err_ptr, h)
+                      int(sc.min_select), idx_tmp.data_ptr(), n_tmp.data_ptr(), self.err_ptr,
+                      self.row_range.data_ptr(), h)
 
         def attend():
             if self.resident:
@@ -1176,7 +1180,7 @@ class DecodeEngine:
             _lib.call("ig_rehearse_count", q_ptr, ldq, cols.data_ptr(), self.pk[li - 1].data_ptr(),
                       self.st.data_ptr(), B, Hg, dq, kc, S, self.scale, float(sc.alpha),
                       self.scores.data_ptr(), self.maxkey.data_ptr(), self.rtickets.data_ptr(),
-                      counts.data_ptr(), csum.data_ptr(), cs)
+                      counts.data_ptr(), csum.data_ptr(), self.row_range.data_ptr(), cs)
             if extra_counts is not None:
                 csum += torch.as_tensor(np.asarray(extra_counts, np.int32), device=self.device)
             idx = torch.zeros((B, Hg, self.cap), dtype=torch.int32, device=self.device)
@@ -1184,7 +1188,7 @@ class DecodeEngine:
             err = torch.zeros(1, dtype=torch.int32, device=self.device)
             _lib.call("ig_select", self.scores.data_ptr(), csum.data_ptr(), self.st.data_ptr(), B, Hg,
                       self.H, S, self.cap, float(sc.cap_ratio), int(sc.min_select), idx.data_ptr(),
-                      n.data_ptr(), err.data_ptr(), cs)
+                      n.data_ptr(), err.data_ptr(), self.row_range.data_ptr(), cs)
             out = {"scores": self.scores[:, :, :s].cpu().numpy(), "counts": counts.cpu().numpy(),
                    "count_sum": csum.cpu().numpy(), "n": n.cpu().numpy(), "idx": idx.cpu().numpy()}
         torch.cuda.current_stream(self.device).wait_stream(C)
@@ -1413,7 +1417,8 @@ class DecodeEngine:
                                   self.st.data_ptr(), B, Hg, d, self.kcols, self.S_max,
                                   self.scale, float(sc.alpha), self.scores.data_ptr(),
                                   self.maxkey.data_ptr(), self.rtickets.data_ptr(),
-                                  self.counts.data_ptr(), self.count_sum[nxt].data_ptr(), sps)
+                                  self.counts.data_ptr(), self.count_sum[nxt].data_ptr(),
+                                  self.row_range.data_ptr(), sps)
                         self._mark("rehearse", nxt, SP, False)
                         self._mark("select", nxt, SP, True)
                         if self.peer_cnt is not None:
@@ -1433,13 +1438,13 @@ class DecodeEngine:
                                       self.slot_id[nxt - 1].data_ptr(),
                                       self.slot_used[nxt - 1].data_ptr(), self.frow[par].data_ptr(),
                                       self.fslot[par].data_ptr(), self.fcount[par].data_ptr(),
-                                      self.moved_rows[nxt].data_ptr(), sps)
+                                      self.moved_rows[nxt].data_ptr(), self.row_range.data_ptr(), sps)
                         else:
                             _lib.call("ig_select", self.scores.data_ptr(),
                                       self.count_sum[nxt].data_ptr(), self.st.data_ptr(), B, Hg,
                                       self.H, self.S_max, self.cap, float(sc.cap_ratio),
                                       int(sc.min_select), self.idx[nxt].data_ptr(),
-                                      self.n[nxt].data_ptr(), self.err_ptr, sps)
+                                      self.n[nxt].data_ptr(), self.err_ptr, self.row_range.data_ptr(), sps)
                         self._mark("select", nxt, SP, False)
                         if cfg.record_scores:
                             spec_scores[nxt] = self.scores[:, :, :s].cpu()

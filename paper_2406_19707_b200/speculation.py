@@ -206,7 +206,7 @@ def select_tokens(scores: list, cfg: SpeculationConfig):
               counts.data_ptr(), csum.data_ptr(), hs)
     _lib.call("ig_select", sc.data_ptr(), csum.data_ptr(), st.data_ptr(), 1, H, H, S, cap,
               float(cfg.cap_ratio), int(cfg.min_select), idx.data_ptr(), n.data_ptr(),
-              err.data_ptr(), hs)
+              err.data_ptr(), None, hs)
     _lib.call("ig_order_by_score", sc.data_ptr(), n.data_ptr(), 1, H, S, cap, idx.data_ptr(), hs)
     if int(err.item()):
         raise RuntimeError("selection exceeded its index buffer")

@@ -39,7 +39,7 @@ def test_every_declared_symbol_is_exported_and_bound(lib):
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.ig_abi_version() == 1
+    assert lib.ig_abi_version() == 2
     assert lib.ig_status_string(0) == b"ok"
     assert b"invalid" in lib.ig_status_string(1)
 
@@ -48,7 +48,7 @@ def test_argument_validation_without_gpu(lib):
     from paper_2406_19707_b200 import _lib
     P = None
     assert lib.ig_rehearse(P, 0, P, P, P, 0, 1, 1, 1, 4, 1.0, P, P, P) == _lib.IG_EINVAL
-    assert lib.ig_select(P, P, P, 1, 1, 1, 4, 1, 0.2, 1, P, P, P, P) == _lib.IG_EINVAL
+    assert lib.ig_select(P, P, P, 1, 1, 1, 4, 1, 0.2, 1, P, P, P, None, P) == _lib.IG_EINVAL
     assert lib.ig_fetch(P, P, P, 1, 1, 4, 1, 512, P, 1, 256, P) == _lib.IG_EINVAL
     assert lib.ig_attend(P, 0, P, P, 0, P, 0, P, P, P, P, 1, 1, 128, 4, P, P, P, 0, P) == _lib.IG_EINVAL
     assert lib.ig_count(P, P, P, 1, 1, 4, -1.0, P, P, P) == _lib.IG_EINVAL

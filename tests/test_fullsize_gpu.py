@@ -65,9 +65,10 @@ def test_layer_pipeline_full_size(name, B, Hg, s):
     mk = torch.zeros((B, Hg), dtype=torch.int32, device=dev)
     tk0 = torch.zeros((B, Hg), dtype=torch.int32, device=dev)
     scale = float(np.float32(1.0 / np.sqrt(d)))
+    rr = torch.zeros((B, Hg, 2), dtype=torch.int32, device=dev)
     _lib.call("ig_rehearse_count", qspec.data_ptr(), Hg * d, cols.data_ptr(), pk.data_ptr(),
               st.data_ptr(), B, Hg, d, k, S, scale, ALPHA, scores.data_ptr(), mk.data_ptr(),
-              tk0.data_ptr(), counts.data_ptr(), csum.data_ptr(), hs)
+              tk0.data_ptr(), counts.data_ptr(), csum.data_ptr(), rr.data_ptr(), hs)
     assert not mk.any() and not tk0.any()      # scratch left zeroed
     qsel = torch.gather(qspec.view(B, Hg, d).double(), 2, cols.long())           # [B, Hg, k]
     ref = torch.einsum("bhj,bhjt->bht", qsel, pk[..., :s].double()) * scale
@@ -86,8 +87,16 @@ def test_layer_pipeline_full_size(name, B, Hg, s):
     idx = torch.zeros(B, Hg, cap, dtype=torch.int32, device=dev)
     n = torch.zeros(B, dtype=torch.int32, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
+    # with the rehearsal's row ranges, and computing them itself: identical
+    idx2 = torch.full_like(idx, -7)
+    n2 = torch.zeros_like(n)
     _lib.call("ig_select", scores.data_ptr(), csum.data_ptr(), st.data_ptr(), B, Hg, H_total, S,
-              cap, CAP_RATIO, 1, idx.data_ptr(), n.data_ptr(), err.data_ptr(), hs)
+              cap, CAP_RATIO, 1, idx.data_ptr(), n.data_ptr(), err.data_ptr(), rr.data_ptr(), hs)
+    _lib.call("ig_select", scores.data_ptr(), csum.data_ptr(), st.data_ptr(), B, Hg, H_total, S,
+              cap, CAP_RATIO, 1, idx2.data_ptr(), n2.data_ptr(), err.data_ptr(), None, hs)
+    assert torch.equal(n, n2)
+    for b in range(B):
+        assert torch.equal(idx[b, :, :int(n[b])], idx2[b, :, :int(n[b])])
     n_np, idx_np, cs = n.cpu().numpy(), idx.cpu().numpy(), csum.cpu().numpy()
     assert int(err.item()) == 0
     for b in range(B):

@@ -62,6 +62,12 @@ def test_select_tokens_random_with_ties(seed):
             np.testing.assert_array_equal(got_p[h], ref_p[h])
 
 
+def _order_keys(x: np.ndarray) -> np.ndarray:
+    """The kernels' order-preserving u32 keys (-0.0 keyed as +0.0)."""
+    u = np.where(x == 0, np.float32(0), x).astype(np.float32).view(np.uint32)
+    return np.where(u & 0x80000000, ~u, u | 0x80000000).astype(np.uint32)
+
+
 def _select_direct(sc: np.ndarray, cfg):
     """ig_select on [H, s] scores with the reference's head counts: (n, [H] ascending rows)."""
     import math
@@ -81,7 +87,7 @@ def _select_direct(sc: np.ndarray, cfg):
     err = torch.zeros(1, dtype=torch.int32, device="cuda")
     _lib.call("ig_select", dsc.data_ptr(), csum.data_ptr(), st.data_ptr(), 1, H, H, S, cap,
               float(cfg.cap_ratio), int(cfg.min_select), idx.data_ptr(), n.data_ptr(), err.data_ptr(),
-              _lib.stream_handle())
+              None, _lib.stream_handle())
     assert int(err.item()) == 0
     nn = int(n.item())
     got = idx[0].cpu().numpy()
@@ -247,11 +253,16 @@ def test_rehearse_count_fused_matches_oracle(s):
     tq = torch.from_numpy(qspec).to(dev)
     tc = torch.from_numpy(cols.astype(np.int32)).to(dev)
     scale = float(np.float32(1.0 / np.sqrt(d)))
+    rr = torch.zeros((B, Hg, 2), dtype=torch.int32, device=dev)
     _lib.call("ig_rehearse_count", tq.data_ptr(), Hg * d, tc.data_ptr(), pk.data_ptr(), st.data_ptr(),
               B, Hg, d, k, S, scale, alpha, scores.data_ptr(), mk.data_ptr(), tk.data_ptr(),
-              counts.data_ptr(), csum.data_ptr(), _lib.stream_handle())
+              counts.data_ptr(), csum.data_ptr(), rr.data_ptr(), _lib.stream_handle())
     assert not mk.any() and not tk.any()          # scratch left zeroed
     got_s = scores.cpu().numpy()[..., :s]
+    # row_range: the (max, min) order keys of each row's s scores
+    keys = _order_keys(got_s)
+    np.testing.assert_array_equal(rr.cpu().numpy().view(np.uint32),
+                                  np.stack([keys.max(-1), keys.min(-1)], -1))
     got_c = counts.cpu().numpy()
     for b in range(B):
         arts = O.Partials(2, Hg)

@@ -389,9 +389,9 @@ def test_select_plan_fused_equals_two_launches(S, cap, B, Hg):
                 idx.data_ptr(), n.data_ptr(), err.data_ptr())
         if fused:
             _lib.call("ig_select_plan", *args, pos.data_ptr(), slot.data_ptr(), used.data_ptr(), frow.data_ptr(),
-                      fslot.data_ptr(), fcount.data_ptr(), moved.data_ptr(), _lib.stream_handle())
+                      fslot.data_ptr(), fcount.data_ptr(), moved.data_ptr(), None, _lib.stream_handle())
         else:
-            _lib.call("ig_select", *args, _lib.stream_handle())
+            _lib.call("ig_select", *args, None, _lib.stream_handle())
             _lib.call("ig_resident_plan", idx.data_ptr(), n.data_ptr(), pos.data_ptr(), slot.data_ptr(),
                       used.data_ptr(), B, Hg, cap, frow.data_ptr(), fslot.data_ptr(), fcount.data_ptr(),
                       moved.data_ptr(), _lib.stream_handle())
