@@ -369,6 +369,48 @@ __device__ __forceinline__ int select_row(const float* __restrict__ scores, cons
     need_eq = nd;
   }
   int a = 0, e = 0;
+  // short rows, no tie cut: the warp compacts the rows of bins <= b* of its
+  // range into shared memory as it counts them (b* rows flagged in bit 31),
+  // so P3 is a copy of those entries instead of a second pass over the row
+  constexpr bool kCompact = THREADS <= 512;
+  int32_t* wbuf = reinterpret_cast<int32_t*>(bits + (S_max + 31) / 32) + t_lo;
+  int wcount = 0;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  if (kCompact && mode != 2) {
+    for (int t0 = t_lo; t0 < t_hi; t0 += 128) {
+      const int t = t0 + lane * 4;
+      int bn[4] = {kBins, kBins, kBins, kBins};
+      float x[4] = {0.f, 0.f, 0.f, 0.f};
+      if (t < t_hi) {
+        const float4 v = row4(row, t);
+        x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (t + i < t_hi) bn[i] = vbin(x[i], hi, scale);
+      }
+      int before = 0, total = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const unsigned mb = __ballot_sync(0xffffffffu, bn[i] <= bstar);
+        before += __popc(mb & lt_mask);
+        total += __popc(mb);
+      }
+      int pos = wcount + before;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (bn[i] < bstar || (bn[i] == bstar && mode == 0)) {
+          ++a;
+          wbuf[pos++] = t + i;
+        } else if (bn[i] == bstar) {
+          wbuf[pos++] = (t + i) | (int)0x80000000;
+          const int slot = atomicAdd(&sh.ncand, 1);
+          sh.cand_key[slot] = order_key(x[i]);
+          sh.cand_t[slot] = t + i;
+        }
+      }
+      wcount += total;
+    }
+  } else
   for (int t = t_lo + lane * 4; t < t_hi; t += 128) {
     const float4 v = row4(row, t);
     const float x[4] = {v.x, v.y, v.z, v.w};
@@ -418,7 +460,19 @@ __device__ __forceinline__ int select_row(const float* __restrict__ scores, cons
 
   // ---- P3: ascending emission
   int out_off = 0, eq_before = 0;
-  const unsigned lt_mask = (1u << lane) - 1u;
+  if (kCompact && mode != 2) {
+    out_off = warp_sum(lane < w ? sh.warp_a[lane] : 0);      // rows of the warps before mine
+    for (int j0 = 0; j0 < wcount; j0 += 32) {
+      const int j = j0 + lane;
+      const int ent = j < wcount ? wbuf[j] : 0;
+      const int t = ent & 0x7fffffff;
+      const bool take = j < wcount && (ent >= 0 || ((bits[t >> 5] >> (t & 31)) & 1u));
+      const unsigned mb = __ballot_sync(0xffffffffu, take);
+      if (take) out[out_off + __popc(mb & lt_mask)] = t;
+      out_off += __popc(mb);
+    }
+    return nn;
+  }
   if (mode != 2) {
     out_off = warp_sum(lane < w ? sh.warp_a[lane] : 0);      // rows of the warps before mine
     // no tie cut inside b*: a row is taken iff its bin is < b*, or == b* and
@@ -522,7 +576,7 @@ __device__ __forceinline__ int select_row(const float* __restrict__ scores, cons
 // of the same (b, h) runs in the same CTA on the selection just written --
 // one launch and one dependent hop fewer on the speculation chain)
 template <int THREADS, bool PLAN>
-__global__ void __launch_bounds__(THREADS) __maxnreg__(THREADS == 1024 ? 64 : 32)   // 1024: no spills at C4 row lengths
+__global__ void __launch_bounds__(THREADS) __maxnreg__(THREADS == 1024 ? 64 : THREADS == 256 ? 40 : 32)   // no spills; 256: 6 CTAs/SM
 select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ count_sum,
               const ig_step_state* __restrict__ st, int Hg, int H_total, int S_max, int cap_max,
               double cap_ratio, int min_select, int32_t* __restrict__ idx,
@@ -536,7 +590,8 @@ select_kernel(const float* __restrict__ scores, const int32_t* __restrict__ coun
                                     idx, n_out, err_flag, row_range, sh, bits);
   if constexpr (PLAN) {
     const size_t bh = (size_t)blockIdx.y * Hg + blockIdx.x;
-    int32_t* freelist = reinterpret_cast<int32_t*>(bits + (S_max + 31) / 32);
+    // after the take bitmap and the compaction buffer (short-row kernels)
+    int32_t* freelist = reinterpret_cast<int32_t*>(bits + (S_max + 31) / 32) + (THREADS <= 512 ? S_max : 0);
     uint8_t* matched = reinterpret_cast<uint8_t*>(freelist + cap_max);
     __syncthreads();                  // the selection (global) and the bitmap reads are done
     plan_row(idx + bh * cap_max, n, pos_prev ? pos_prev[bh] : -1, slot_id + bh * cap_max, slot_used + bh,
@@ -596,7 +651,9 @@ static int select_launch(const float* scores, const int32_t* count_sum, const ig
   const bool plan = slot_id != nullptr;
   if (plan && (!slot_used || !frow || !fslot || !fcount)) return IG_EINVAL;
   // the take bitmap (+ the plan's free list and match flags)
-  const size_t smem = (size_t)(S_max + 31) / 32 * 4 + (plan ? (size_t)cap_max * 5 : 0);
+  const bool short_rows = S_max <= kSelLongRows;
+  const size_t smem = (size_t)(S_max + 31) / 32 * 4 + (short_rows ? (size_t)S_max * 4 : 0) +
+                      (plan ? (size_t)cap_max * 5 : 0);
   if (smem > 200 * 1024) return IG_EINVAL;
   // rows up to kSelLongRows: 256 threads (5 CTAs/SM: C3's 640 rows in one wave);
   // IG_SELECT_THREADS=512 for the A/B
