@@ -454,6 +454,10 @@ class DecodeEngine:
         # IG_APPEND_FIRST=1: launch ig_append(li) before releasing the speculation
         # chain of li+1 (measured at C3: 952 vs 984 tok/s -- off)
         self.append_first = os.environ.get("IG_APPEND_FIRST", "0") == "1"
+        # IG_SELECT_AFTER_ATTEND=1: the select / plan / fetch of layer li+1 wait for
+        # attend(li), so the latency-bound select does not hold SM slots the
+        # attention needs -- measured 946 vs 998 tok/s at C3 (profiles/r02saa_*): off
+        self.select_after_attend = os.environ.get("IG_SELECT_AFTER_ATTEND", "0") == "1"
         self.scale = float(np.float32(1.0 / np.sqrt(d)))   # speculation.py:127
         self._load_weights(model)
         self._alloc()
@@ -1397,6 +1401,7 @@ class DecodeEngine:
                     if AP is not C:
                         self.ev_app[li].record(AP)
                 appended = False
+                deferred = None
                 nxt = li + 1
                 if nxt < L:
                     if speculative:
@@ -1420,64 +1425,73 @@ class DecodeEngine:
                                   self.counts.data_ptr(), self.count_sum[nxt].data_ptr(),
                                   self.row_range.data_ptr(), sps)
                         self._mark("rehearse", nxt, SP, False)
-                        self._mark("select", nxt, SP, True)
-                        if self.peer_cnt is not None:
-                            self.peer_cnt(self.count_sum[nxt], self.count_sum[nxt], None, self.st,
-                                          nxt - 1, L - 1, sps)
-                        elif self.world > 1:
-                            with torch.cuda.stream(SP):
-                                dist.all_reduce(self.count_sum[nxt], group=self.group)
-                        par = nxt % 2
-                        if resident and self.fuse_plan:
-                            # select + resident plan of each (b, h) in one CTA
-                            _lib.call("ig_select_plan", self.scores.data_ptr(),
-                                      self.count_sum[nxt].data_ptr(), self.st.data_ptr(), B, Hg,
-                                      self.H, self.S_max, self.cap, float(sc.cap_ratio),
-                                      int(sc.min_select), self.idx[nxt].data_ptr(),
-                                      self.n[nxt].data_ptr(), self.err_ptr, self.pos[nxt].data_ptr(),
-                                      self.slot_id[nxt - 1].data_ptr(),
-                                      self.slot_used[nxt - 1].data_ptr(), self.frow[par].data_ptr(),
-                                      self.fslot[par].data_ptr(), self.fcount[par].data_ptr(),
-                                      self.moved_rows[nxt].data_ptr(), self.row_range.data_ptr(), sps)
+                        def spec_tail(nxt=nxt):
+                            """select / plan / fetch of layer nxt (spec and fetch streams)"""
+                            par = nxt % 2
+                            self._mark("select", nxt, SP, True)
+                            if self.peer_cnt is not None:
+                                self.peer_cnt(self.count_sum[nxt], self.count_sum[nxt], None, self.st,
+                                              nxt - 1, L - 1, sps)
+                            elif self.world > 1:
+                                with torch.cuda.stream(SP):
+                                    dist.all_reduce(self.count_sum[nxt], group=self.group)
+                            par = nxt % 2
+                            if resident and self.fuse_plan:
+                                # select + resident plan of each (b, h) in one CTA
+                                _lib.call("ig_select_plan", self.scores.data_ptr(),
+                                          self.count_sum[nxt].data_ptr(), self.st.data_ptr(), B, Hg,
+                                          self.H, self.S_max, self.cap, float(sc.cap_ratio),
+                                          int(sc.min_select), self.idx[nxt].data_ptr(),
+                                          self.n[nxt].data_ptr(), self.err_ptr, self.pos[nxt].data_ptr(),
+                                          self.slot_id[nxt - 1].data_ptr(),
+                                          self.slot_used[nxt - 1].data_ptr(), self.frow[par].data_ptr(),
+                                          self.fslot[par].data_ptr(), self.fcount[par].data_ptr(),
+                                          self.moved_rows[nxt].data_ptr(), self.row_range.data_ptr(), sps)
+                            else:
+                                _lib.call("ig_select", self.scores.data_ptr(),
+                                          self.count_sum[nxt].data_ptr(), self.st.data_ptr(), B, Hg,
+                                          self.H, self.S_max, self.cap, float(sc.cap_ratio),
+                                          int(sc.min_select), self.idx[nxt].data_ptr(),
+                                          self.n[nxt].data_ptr(), self.err_ptr, self.row_range.data_ptr(), sps)
+                            self._mark("select", nxt, SP, False)
+                            if cfg.record_scores:
+                                spec_scores[nxt] = self.scores[:, :, :s].cpu()
+                            if resident and not self.fuse_plan:
+                                _lib.call("ig_resident_plan", self.idx[nxt].data_ptr(),
+                                          self.n[nxt].data_ptr(), self.pos[nxt].data_ptr(),
+                                          self.slot_id[nxt - 1].data_ptr(),
+                                          self.slot_used[nxt - 1].data_ptr(), B, Hg, self.cap,
+                                          self.frow[par].data_ptr(), self.fslot[par].data_ptr(),
+                                          self.fcount[par].data_ptr(),
+                                          self.moved_rows[nxt].data_ptr(), sps)
+                            self.ev_sel[nxt].record(SP)
+                            Fs.wait_event(self.ev_sel[nxt])
+                            self._mark("fetch", nxt, Fs, True)
+                            if resident:
+                                _lib.call("ig_fetch_slots", self._pool_layer_dev(nxt),
+                                          self.frow[par].data_ptr(), self.fslot[par].data_ptr(),
+                                          self.fcount[par].data_ptr(), B, Hg, self.S_max, self.cap,
+                                          self.row_bytes, self.stage_res[nxt - 1].data_ptr(),
+                                          Fs.cuda_stream)
+                            elif self.fetch_impl == "tma":
+                                _lib.call("ig_fetch_tma", self._pool_layer_dev(nxt),
+                                          self.idx[nxt].data_ptr(), self.n[nxt].data_ptr(), None, B,
+                                          Hg, self.S_max, self.cap, self.row_bytes,
+                                          self.stage_sel[nxt % 2].data_ptr(), self.fetch_ctas,
+                                          max(1, self.fetch_threads // 32), self.fetch_rows,
+                                          Fs.cuda_stream)
+                            else:
+                                _lib.call("ig_fetch", self._pool_layer_dev(nxt), self.idx[nxt].data_ptr(),
+                                          self.n[nxt].data_ptr(), B, Hg, self.S_max, self.cap,
+                                          self.row_bytes, self.stage_sel[nxt % 2].data_ptr(),
+                                          self.fetch_ctas, self.fetch_threads, Fs.cuda_stream)
+                            self._mark("fetch", nxt, Fs, False)
+                            self.ev_fetch[nxt].record(Fs)
+
+                        if self.select_after_attend:
+                            deferred = spec_tail     # launched behind attend(li), below
                         else:
-                            _lib.call("ig_select", self.scores.data_ptr(),
-                                      self.count_sum[nxt].data_ptr(), self.st.data_ptr(), B, Hg,
-                                      self.H, self.S_max, self.cap, float(sc.cap_ratio),
-                                      int(sc.min_select), self.idx[nxt].data_ptr(),
-                                      self.n[nxt].data_ptr(), self.err_ptr, self.row_range.data_ptr(), sps)
-                        self._mark("select", nxt, SP, False)
-                        if cfg.record_scores:
-                            spec_scores[nxt] = self.scores[:, :, :s].cpu()
-                        if resident and not self.fuse_plan:
-                            _lib.call("ig_resident_plan", self.idx[nxt].data_ptr(),
-                                      self.n[nxt].data_ptr(), self.pos[nxt].data_ptr(),
-                                      self.slot_id[nxt - 1].data_ptr(),
-                                      self.slot_used[nxt - 1].data_ptr(), B, Hg, self.cap,
-                                      self.frow[par].data_ptr(), self.fslot[par].data_ptr(),
-                                      self.fcount[par].data_ptr(),
-                                      self.moved_rows[nxt].data_ptr(), sps)
-                        self.ev_sel[nxt].record(SP)
-                        Fs.wait_event(self.ev_sel[nxt])
-                        self._mark("fetch", nxt, Fs, True)
-                        if resident:
-                            _lib.call("ig_fetch_slots", self._pool_layer_dev(nxt),
-                                      self.frow[par].data_ptr(), self.fslot[par].data_ptr(),
-                                      self.fcount[par].data_ptr(), B, Hg, self.S_max, self.cap,
-                                      self.row_bytes, self.stage_res[nxt - 1].data_ptr(),
-                                      Fs.cuda_stream)
-                        elif self.fetch_impl == "tma":
-                            _lib.call("ig_fetch_tma", self._pool_layer_dev(nxt),
-                                      self.idx[nxt].data_ptr(), self.n[nxt].data_ptr(), None, B,
-                                      Hg, self.S_max, self.cap, self.row_bytes,
-                                      self.stage_sel[nxt % 2].data_ptr(), self.fetch_ctas,
-                                      max(1, self.fetch_threads // 32), self.fetch_rows,
-                                      Fs.cuda_stream)
-                        else:
-                            _lib.call("ig_fetch", self._pool_layer_dev(nxt), self.idx[nxt].data_ptr(),
-                                      self.n[nxt].data_ptr(), B, Hg, self.S_max, self.cap,
-                                      self.row_bytes, self.stage_sel[nxt % 2].data_ptr(),
-                                      self.fetch_ctas, self.fetch_threads, Fs.cuda_stream)
-                        self._mark("fetch", nxt, Fs, False)
+                            spec_tail()
                     else:
                         if li >= 1:
                             Fs.wait_event(self.ev_att[li - 1])
@@ -1487,7 +1501,7 @@ class DecodeEngine:
                             self._issue_full_fetch_dev(nxt, self.stage_full[nxt % 2])
                         else:
                             self._issue_full_fetch(nxt, s, self.stage_full[nxt % 2])
-                    self.ev_fetch[nxt].record(Fs)
+                        self.ev_fetch[nxt].record(Fs)
                 if not (speculative and nxt < L):      # else computed by the fused GEMM
                     self._gemm(self.x_a, self.wqkv[li], self.qkv, cs)
                 if not appended:
@@ -1506,6 +1520,10 @@ class DecodeEngine:
                     self._attend(li, stage, None, None, self.S_max, cs, apos)
                 self._mark("attend", li, C, False)
                 self.ev_att[li].record(C)
+                if deferred is not None:            # IG_SELECT_AFTER_ATTEND
+                    SP.wait_event(self.ev_att[li])
+                    deferred()
+                    deferred = None
                 if self.world > 1:
                     if self.peer_ar is not None and self.peer_fuse:
                         # the GEMM epilogue pushes into every rank; x_mid = x + sum
