@@ -110,6 +110,7 @@ struct PeerOut {
   const ig_step_state* st = nullptr;
   uint32_t* done = nullptr;          // grid-completion counter (local, left zeroed)
   int rank = 0, world = 1, call = 0, calls = 1;
+  int l2pf = 0;                      // prefetch this CTA's blocks beyond the ring into L2 (IG_PACKED_L2PF)
 };
 
 // chunk index -> CTA that owns it, for the split [c T / G, (c+1) T / G)
@@ -157,8 +158,16 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
     bulk_g2s(ring_s + st * kBlockFloats * 4, P + (size_t)(g0 + jj) * kBlockFloats,
              kBlockFloats * 4, full_s + 8 * st);
   };
-  if (tid == 0)
+  if (tid == 0) {
     for (int jj = 0; jj < kStages && g0 + jj < g1; ++jj) issue(jj, jj);
+    // small GEMMs (few blocks per CTA): the rest of this CTA's blocks into L2
+    // while the previous kernel drains
+    if (g1 - g0 <= po.l2pf)
+      for (int jj = kStages; g0 + jj < g1; ++jj)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P + (size_t)(g0 + jj) * kBlockFloats),
+                     "r"(kBlockFloats * 4)
+                     : "memory");
+  }
   // Programmatic dependent launch: the weight stream above does not depend on
   // the previous kernel, so this grid may start (and fill its rings) while
   // that kernel drains; x, R, Y, the workspace and the tickets are touched
@@ -474,6 +483,16 @@ inline int packed_cta_mode() {
   return m == 16 || m == 8 ? m : 0;
 }
 
+// IG_PACKED_L2PF=N: a CTA with <= N blocks prefetches the ones beyond its ring
+// into L2 before griddepcontrol.wait (A/B; 0 = off)
+inline int packed_l2pf() {
+  static const int n = [] {
+    const char* e = getenv("IG_PACKED_L2PF");
+    return e ? atoi(e) : 0;
+  }();
+  return n;
+}
+
 inline int ctas_per_sm(int M) {
   // IG_PACKED_CTA=16: one 16-warp CTA per SM with a 6-deep ring (more bytes in
   // flight, fewer CTA fix-ups) -- measured equal or slower (ffn_out 4.7 vs 5.6
@@ -500,8 +519,10 @@ int launch(const float* X, int ldx, const float* P, float* Y, int ldy, const flo
   attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  PeerOut pl = po;
+  pl.l2pf = packed_l2pf();
   IG_CUDA_STATUS(cudaLaunchKernelEx(&cfg, kern, X, ldx, P, Y, ldy, R, ldr, M, N, K, C, epilogue, ws,
-                                    tickets, po));
+                                    tickets, pl));
   IG_LAUNCH_STATUS();
   return IG_OK;
 }
