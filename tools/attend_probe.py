@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--heads", type=int, default=40)
     ap.add_argument("--ctx", type=int, default=4096)
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--sweep", type=str, default="",
+                    help="comma-separated row counts at the 20%% cap (fixed-cost fit), e.g. 16,256,819")
     ap.add_argument("--chain", type=int, default=10,
                     help="launches back to back between one event pair (amortises host launch cost)")
     a = ap.parse_args()
@@ -28,8 +30,11 @@ def main():
     B, Hg, d = a.batch, a.heads, 128
     g = torch.Generator(device="cuda")
     g.manual_seed(0)
-    for name, rows, cap in (("layer>=1 (n = 20% cap)", a.ctx // 5, a.ctx // 5 + 1),
-                            ("layer 0 (all rows)", a.ctx, a.ctx + 4)):
+    cases = [("layer>=1 (n = 20% cap)", a.ctx // 5, a.ctx // 5 + 1),
+             ("layer 0 (all rows)", a.ctx, a.ctx + 4)]
+    if a.sweep:
+        cases = [(f"sweep rows {r}", int(r), a.ctx // 5 + 1) for r in a.sweep.split(",")]
+    for name, rows, cap in cases:
         q = torch.randn(B, 3 * Hg * d, device="cuda", generator=g)
         stage = torch.randn(B, Hg, cap, 2 * d, device="cuda", generator=g).half()
         n = torch.full((B,), rows, dtype=torch.int32, device="cuda")
