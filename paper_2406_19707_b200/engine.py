@@ -448,6 +448,7 @@ class DecodeEngine:
         # without record_selection / record_scores -- what the reference's run()
         # always keeps (one host sync per layer: a trace mode, not the perf path)
         self.record_trace = bool(record_trace)
+        self._out_host = None           # step_host's pinned output rows
         # IG_FUSE_PLAN=1: the resident plan fused into the select (ig_select_plan) --
         # measured 967 vs 989 tok/s at C3 (profiles/r02aa_*), so two launches by default
         self.fuse_plan = os.environ.get("IG_FUSE_PLAN", "0") == "1"
@@ -1642,9 +1643,13 @@ class DecodeEngine:
         if x_host is not None:
             self.x.copy_(torch.from_numpy(np.ascontiguousarray(x_host, np.float32)).reshape(self.B, self.D),
                          non_blocking=True)
-        out = self.decode_step().cpu().numpy()
+        y = self.decode_step()
+        if self._out_host is None:      # pinned: one DMA, no pageable staging per step
+            self._out_host = torch.empty(y.shape, dtype=y.dtype).pin_memory()
+        self._out_host.copy_(y, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
         self.check_errors()
-        return out
+        return self._out_host.numpy().copy()
 
     def trace(self) -> dict:
         """Schema-v1 trace (engine.py:83-196; selected lists are ascending)."""

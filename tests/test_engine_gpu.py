@@ -665,3 +665,35 @@ def test_cuda_graph_replay_is_identical(rname, pool):
     np.testing.assert_array_equal(meta[0][0], meta[1][0])
     np.testing.assert_array_equal(meta[0][1], meta[1][1])
     assert meta[0][2:] == meta[1][2:]
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_step_host_matches_decode_step(graph):
+    """The end-to-end API (host rows in, host rows out, pinned output buffer)
+    returns exactly what decode_step leaves on the device, and a fresh array
+    each step (not a view of the engine's pinned buffer)."""
+    import torch
+    from paper_2406_19707_b200 import DecodeEngine
+    plain, sk = models("m256")
+    ocfg = run_config("spec", gen_len=4)
+    sessions = oracle_sessions(sk, ocfg)
+    outs, host_seq = [], None
+    for api in ("device", "host"):
+        eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg, record_selection=False),
+                                         copy.deepcopy(sessions), cuda_graph=graph)
+        try:
+            x = eng.x.cpu().numpy()
+            seq = []
+            for _ in range(ocfg.gen_len):
+                if api == "device":
+                    eng.x.copy_(torch.from_numpy(x))
+                    x = eng.decode_step().cpu().numpy()
+                else:
+                    x = eng.step_host(torch.from_numpy(x).pin_memory().numpy())
+                seq.append(x)
+            outs.append(np.stack(seq))
+            host_seq = seq
+        finally:
+            eng.close()
+    np.testing.assert_array_equal(outs[0], outs[1])
+    assert not np.shares_memory(host_seq[0], host_seq[1])
