@@ -1637,13 +1637,23 @@ class DecodeEngine:
                 r["spec_scores"] = spec_scores[li][b].numpy()     # [Hg, s]; lists in trace()
             recs[b][li] = r
 
-    def step_host(self, x_host: np.ndarray | None = None) -> np.ndarray:
+    def step_host(self, x_host: np.ndarray | None = None, out: np.ndarray | None = None) -> np.ndarray:
         """End-to-end API: optional host input row(s) in, host output rows out
-        (the reference decode_step returns the output row, engine.py:380)."""
+        (the reference decode_step returns the output row, engine.py:380).
+        out: optional [B, D] float32 array that receives the rows (a pinned one
+        takes one direct DMA; it may be x_host itself -- the copy in is ordered
+        before the copy out); else a fresh array is returned."""
         if x_host is not None:
             self.x.copy_(torch.from_numpy(np.ascontiguousarray(x_host, np.float32)).reshape(self.B, self.D),
                          non_blocking=True)
         y = self.decode_step()
+        if out is not None:
+            if out.shape != (self.B, self.D) or out.dtype != np.float32 or not out.flags.c_contiguous:
+                raise ValueError(f"out must be a C-contiguous float32 [{self.B}, {self.D}] array")
+            torch.from_numpy(out).copy_(y, non_blocking=True)
+            torch.cuda.current_stream(self.device).synchronize()
+            self.check_errors()
+            return out
         if self._out_host is None:      # pinned: one DMA, no pageable staging per step
             self._out_host = torch.empty(y.shape, dtype=y.dtype).pin_memory()
         self._out_host.copy_(y, non_blocking=True)

@@ -678,7 +678,7 @@ def test_step_host_matches_decode_step(graph):
     ocfg = run_config("spec", gen_len=4)
     sessions = oracle_sessions(sk, ocfg)
     outs, host_seq = [], None
-    for api in ("device", "host"):
+    for api in ("device", "host", "inplace"):
         eng = DecodeEngine.from_sessions(sk, engine_cfg(ocfg, record_selection=False),
                                          copy.deepcopy(sessions), cuda_graph=graph)
         try:
@@ -688,12 +688,18 @@ def test_step_host_matches_decode_step(graph):
                 if api == "device":
                     eng.x.copy_(torch.from_numpy(x))
                     x = eng.decode_step().cpu().numpy()
-                else:
+                elif api == "host":
                     x = eng.step_host(torch.from_numpy(x).pin_memory().numpy())
+                else:                       # in place: the rows go back into the pinned input
+                    xp = torch.from_numpy(x).pin_memory().numpy()
+                    assert eng.step_host(xp, out=xp) is xp
+                    x = xp.copy()
                 seq.append(x)
             outs.append(np.stack(seq))
-            host_seq = seq
+            if api == "host":
+                host_seq = seq
         finally:
             eng.close()
     np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[0], outs[2])
     assert not np.shares_memory(host_seq[0], host_seq[1])
