@@ -270,7 +270,7 @@ def run_b200(a) -> None:
     model = generate_synthetic_gpu(spec, device=dev)
     skew_model_gpu(model)
     # warmup + timed + e2e + (HBM variant: 2 + timed) decode steps, plus slack
-    steps_total = a.warmup + 4 * a.steps + 8
+    steps_total = a.warmup + 4 * a.steps + 16
     cfg = RunConfig(scheme="speculative", prompt_len=a.prompt, gen_len=steps_total, batch=a.batch,
                     speculation=SpeculationConfig(WORKLOAD["ratio"], WORKLOAD["alpha"], WORKLOAD["cap"], 1))
     eng = DecodeEngine(model, cfg, pool_dtype="f16", device=dev, group=group, fetch_ctas=a.fetch_ctas,
@@ -360,6 +360,14 @@ def run_b200(a) -> None:
         eng.step_host(xh, out=xh)       # rows in from pinned memory, the step's rows back into it
     barrier()
     e2e_ms = (time.perf_counter() - t0) * 1000.0
+    # -------- in-graph time of the dense launches (%globaltimer stamps in a re-captured
+    # step: dependency satisfied -> last CTA done; no events between PDL-chained launches)
+    gemm_t = None
+    if a.dense == "packed" and os.environ.get("IG_BENCH_GEMM_TIMING", "1") == "1":
+        try:
+            gemm_t = eng.gemm_timing(3)
+        except Exception as e:  # noqa: BLE001
+            sys.stderr.write(f"bench: in-graph GEMM timing failed ({e!r})\n")
     # -------- secondary variant: resident -> refetch every selected row each
     # step (the reference's data movement, host-link bound); else layer 0 in HBM
     var_ms = 0.0
@@ -452,6 +460,19 @@ def run_b200(a) -> None:
                     "how": "CUDA events around every launch on the compute stream, timed steps"}
         else:
             roof = link_roof
+        if gemm_t and roof.get("kernel", "").startswith("dense"):
+            gb = sum(x["bytes"] for x in gemm_t)
+            gus = sum(x["us"] for x in gemm_t)
+            if gus > 0:
+                roof["in_graph"] = {
+                    "achieved": gb / gus / 1e3, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": gb / gus / 1e3 / hbm_peak, "launches_per_step": len(gemm_t),
+                    "us_per_step": gus, "bytes_per_step": gb,
+                    "step_share": gus / 1e3 / (ms / a.steps),
+                    "how": ("%globaltimer stamps inside ig_sgemm_packed (CTA 0 past its dependency "
+                            "wait -> last CTA done) in the CUDA-graph step, mean of 3 replays: each "
+                            "launch's share of the critical path with PDL (CUDA events between "
+                            "launches would break the PDL chain)")}
         hbm = {}
         for k in ("rehearse_count", "attend", "select", "dense_ffn_in"):   # alone: own roofline
             if k in iso:
