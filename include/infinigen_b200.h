@@ -253,14 +253,6 @@ int ig_sgemm_pack(const float* W, int ldw, int N, int K, float* packed, void* st
 int ig_sgemm_packed(const float* X, int ldx, const float* packed, int N, int K, float* Y, int ldy,
                     const float* R, int ldr, int M, int epilogue, float* workspace,
                     size_t workspace_floats, int32_t* tickets, size_t ntickets, void* stream);
-/* The same launch with in-graph timing for the bench's roofline: stamps[0] =
- * %globaltimer (ns) when CTA 0 passes its dependency wait (the predecessor
- * has completed: PDL), stamps[1] = atomicMax of every CTA's end (set it to 0
- * first).  Measurement only; results identical to ig_sgemm_packed. */
-int ig_sgemm_packed_stamped(const float* X, int ldx, const float* packed, int N, int K, float* Y,
-                            int ldy, const float* R, int ldr, int M, int epilogue, float* workspace,
-                            size_t workspace_floats, int32_t* tickets, size_t ntickets,
-                            uint64_t* stamps, void* stream);
 
 /* ---- head-parallel output all-reduce over peer memory (N > 1) ----------
  * Replaces the NCCL all-reduce of the row-parallel W_O / FFN-out partials

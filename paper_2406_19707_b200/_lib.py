@@ -69,7 +69,6 @@ _SIGS = {
                              _P],
     "ig_allreduce_peer_sum": [_I, _P, _P, _I, _I, _P, _I, _I, _P, _P, _P],
     "ig_sgemm_packed": [_P, _I, _P, _I, _I, _P, _I, _P, _I, _I, _I, _P, _SZ, _P, _SZ, _P],
-    "ig_sgemm_packed_stamped": [_P, _I, _P, _I, _I, _P, _I, _P, _I, _I, _I, _P, _SZ, _P, _SZ, _P, _P],
     "ig_step_advance": [_P, _P],
     "ig_layernorm": [_P, _P, _P, _F, _I, _I, _P, _P],
     "ig_split_f16": [_P, _I, _I, _I, _I, _I, _P, _P, _P],

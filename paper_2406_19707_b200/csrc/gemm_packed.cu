@@ -111,17 +111,7 @@ struct PeerOut {
   uint32_t* done = nullptr;          // grid-completion counter (local, left zeroed)
   int rank = 0, world = 1, call = 0, calls = 1;
   int l2pf = 0;                      // prefetch this CTA's blocks beyond the ring into L2 (IG_PACKED_L2PF)
-  // optional in-graph timing (ig_sgemm_packed_stamped): [0] = %globaltimer when
-  // CTA 0 passes griddepcontrol.wait (the predecessor has completed), [1] = max
-  // over CTAs of their end -- the launch's share of the critical path under PDL
-  unsigned long long* stamps = nullptr;
 };
-
-__device__ __forceinline__ unsigned long long global_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 // chunk index -> CTA that owns it, for the split [c T / G, (c+1) T / G)
 __device__ __forceinline__ int owner(int x, int T, int G) { return (int)(((long)(x + 1) * G - 1) / T); }
@@ -185,7 +175,6 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
   // The next GEMM may likewise launch as soon as SMs free up.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (po.stamps != nullptr && c == 0 && tid == 0) po.stamps[0] = global_ns();
   uint32_t po_epoch = 0;
   size_t po_off = 0;                      // my slot within every rank's receive buffer
   if (po.recv != nullptr) {
@@ -388,10 +377,6 @@ sgemm_packed_kernel(const float* __restrict__ X, int ldx, const float* __restric
     }
     if (tid == 0) tickets[seg_tile] = 0;
     consumers_sync<kWarps * 32>();
-  }
-  if (po.stamps != nullptr) {
-    consumers_sync<kWarps * 32>();
-    if (tid == 0) atomicMax(po.stamps + 1, global_ns());
   }
   if (po.recv != nullptr) {               // every final value of this grid is pushed
     consumers_sync<kWarps * 32>();
@@ -609,18 +594,6 @@ extern "C" int ig_sgemm_packed(const float* X, int ldx, const float* P, int N, i
   return ig::packed::sgemm_packed_any(X, ldx, P, N, K, Y, ldy, R, ldr, M, epilogue, workspace,
                                       workspace_floats, tickets, ntickets, (cudaStream_t)stream,
                                       ig::packed::PeerOut{});
-}
-
-extern "C" int ig_sgemm_packed_stamped(const float* X, int ldx, const float* P, int N, int K,
-                                       float* Y, int ldy, const float* R, int ldr, int M,
-                                       int epilogue, float* workspace, size_t workspace_floats,
-                                       int32_t* tickets, size_t ntickets, uint64_t* stamps,
-                                       void* stream) {
-  if (!Y || !stamps) return IG_EINVAL;
-  ig::packed::PeerOut po;
-  po.stamps = reinterpret_cast<unsigned long long*>(stamps);
-  return ig::packed::sgemm_packed_any(X, ldx, P, N, K, Y, ldy, R, ldr, M, epilogue, workspace,
-                                      workspace_floats, tickets, ntickets, (cudaStream_t)stream, po);
 }
 
 extern "C" int ig_sgemm_packed_peer(const float* X, int ldx, const float* P, int N, int K, int M,

@@ -449,9 +449,6 @@ class DecodeEngine:
         # always keeps (one host sync per layer: a trace mode, not the perf path)
         self.record_trace = bool(record_trace)
         self._out_host = None           # step_host's pinned output rows
-        self._stamps = None             # gemm_timing(): [slots][2] u64 globaltimer stamps
-        self._stamp_i = 0
-        self._stamp_meta = {}
         # IG_FUSE_PLAN=1: the resident plan fused into the select (ig_select_plan) --
         # measured 967 vs 989 tok/s at C3 (profiles/r02aa_*), so two launches by default
         self.fuse_plan = os.environ.get("IG_FUSE_PLAN", "0") == "1"
@@ -1222,18 +1219,6 @@ class DecodeEngine:
             # stream the weights once per 32-row chunk
             for m0 in range(0, M, PACKED_MAX_M):
                 m = min(PACKED_MAX_M, M - m0)
-                stamps = self._stamps
-                if stamps is not None and self._stamp_i < stamps.shape[0]:
-                    # in-graph timing pass (gemm_timing): the same launch, stamped
-                    self._stamp_meta[self._stamp_i] = (m, N, K)
-                    _lib.call("ig_sgemm_packed_stamped", X[m0:].data_ptr(), X.stride(0), P.data_ptr(),
-                              N, K, Y[m0:].data_ptr(), Y.stride(0),
-                              _lib.ptr(R[m0:] if R is not None else None),
-                              R.stride(0) if R is not None else 0, m, epilogue, self.gemm_ws.data_ptr(),
-                              self.gemm_ws.numel(), self.gemm_tickets.data_ptr(),
-                              self.gemm_tickets.numel(), stamps[self._stamp_i].data_ptr(), cs)
-                    self._stamp_i += 1
-                    continue
                 _lib.call("ig_sgemm_packed", X[m0:].data_ptr(), X.stride(0), P.data_ptr(), N, K,
                           Y[m0:].data_ptr(), Y.stride(0), _lib.ptr(R[m0:] if R is not None else None),
                           R.stride(0) if R is not None else 0, m, epilogue, self.gemm_ws.data_ptr(),
@@ -1350,7 +1335,6 @@ class DecodeEngine:
         recs = [[None] * L for _ in range(B)]
         spec_scores = [None] * L
         nar = self._ar_per_layer
-        self._stamp_i = 0
         C.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(C):
             self.count_sum.zero_()
@@ -1652,41 +1636,6 @@ class DecodeEngine:
             if cfg.record_scores and speculative and li >= 1 and spec_scores[li] is not None:
                 r["spec_scores"] = spec_scores[li][b].numpy()     # [Hg, s]; lists in trace()
             recs[b][li] = r
-
-    def gemm_timing(self, steps: int = 3) -> list[dict]:
-        """In-graph time of every packed-GEMM launch of a decode step: the step is
-        re-captured with ig_sgemm_packed_stamped (same kernels, plus %globaltimer
-        stamps: CTA 0 past its dependency wait -> last CTA done, i.e. the launch's
-        share of the critical path with PDL), replayed ``steps`` times (decode steps
-        that advance the state like any other), and per slot the mean over the
-        replays is returned: {"M", "N", "K", "bytes", "us"}.  The plain graph is
-        re-captured on the next decode_step."""
-        if self.dense != "packed":
-            return []
-        self._stamps = torch.zeros((4 * self.L + 8, 2), dtype=torch.int64, device=self.device)
-        self._stamp_meta = {}
-        graph_keep = self.cuda_graph
-        tot = None
-        try:
-            self._graph = None
-            self.decode_step()                 # eager (stamped) + capture when cuda_graph
-            for _ in range(steps):
-                self._stamps[:, 1].zero_()
-                self.decode_step()
-                torch.cuda.synchronize(self.device)
-                st = self._stamps.cpu().numpy().astype(np.int64)
-                d = (st[:, 1] - st[:, 0]) / 1e3
-                tot = d if tot is None else tot + d
-        finally:
-            self._stamps = None
-            self._graph = None
-            self.cuda_graph = graph_keep
-        out = []
-        for i in sorted(self._stamp_meta):
-            M, N, K = self._stamp_meta[i]
-            out.append({"M": M, "N": N, "K": K, "bytes": 4 * (K * N + M * K + M * N),
-                        "us": float(tot[i] / steps)})
-        return out
 
     def step_host(self, x_host: np.ndarray | None = None, out: np.ndarray | None = None) -> np.ndarray:
         """End-to-end API: optional host input row(s) in, host output rows out

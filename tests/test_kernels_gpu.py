@@ -334,40 +334,6 @@ def test_sgemm_packed_vs_float64(M, N, K, epilogue):
     assert not tk.any()
 
 
-def test_sgemm_packed_stamped_is_the_same_launch():
-    """ig_sgemm_packed_stamped (the bench's in-graph GEMM timing) computes exactly
-    what ig_sgemm_packed does and leaves start <= end globaltimer stamps."""
-    import ctypes
-    import torch
-    from paper_2406_19707_b200 import _lib
-    M, N, K = 16, 5120, 5120
-    g = torch.Generator(device="cuda")
-    g.manual_seed(5)
-    X = torch.randn(M, K, device="cuda", generator=g)
-    W = torch.randn(K, N, device="cuda", generator=g)
-    R = torch.randn(M, N, device="cuda", generator=g)
-    pf, wf, tf = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
-    _lib.call("ig_sgemm_packed_sizes", M, N, K, ctypes.byref(pf), ctypes.byref(wf), ctypes.byref(tf),
-              kernels=0)
-    P = torch.empty(pf.value, device="cuda")
-    sh = _lib.stream_handle()
-    _lib.call("ig_sgemm_pack", W.data_ptr(), N, N, K, P.data_ptr(), sh)
-    ws = torch.empty(wf.value, device="cuda")
-    tk = torch.zeros(tf.value, dtype=torch.int32, device="cuda")
-    stamps = torch.zeros(2, dtype=torch.int64, device="cuda")
-    Y0, Y1 = torch.empty(M, N, device="cuda"), torch.empty(M, N, device="cuda")
-    _lib.call("ig_sgemm_packed", X.data_ptr(), K, P.data_ptr(), N, K, Y0.data_ptr(), N, R.data_ptr(), N,
-              M, 2, ws.data_ptr(), ws.numel(), tk.data_ptr(), tk.numel(), sh)
-    _lib.call("ig_sgemm_packed_stamped", X.data_ptr(), K, P.data_ptr(), N, K, Y1.data_ptr(), N,
-              R.data_ptr(), N, M, 2, ws.data_ptr(), ws.numel(), tk.data_ptr(), tk.numel(),
-              stamps.data_ptr(), sh)
-    torch.cuda.synchronize()
-    assert torch.equal(Y0, Y1)
-    t0, t1 = stamps.tolist()
-    assert 0 < t0 < t1 and t1 - t0 < 10_000_000      # ns; one 105-MB GEMM, well under 10 ms
-    assert not tk.any()
-
-
 @pytest.mark.parametrize("elt", ["f16", "bf16"])
 def test_attend_512b_row_variants_match(elt):
     """The two 512-B-row attention kernels -- mma.sync (default) and tcgen05
