@@ -180,3 +180,30 @@ def test_full_width_parity(name):
         eng.close()
     report(name, res)
     assert not problems, problems
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_bench_defaults_are_deterministic(graph):
+    """Three runs of the bench-default engine (f16 pool, resident slot tables,
+    speculation and fetch streams) from the same injected C2 state give the same
+    output bits and selections.  A binary that only shifted the GEMM's timing
+    once broke this (profiles/r02_ab_late/README.md), so it is checked directly."""
+    import torch
+    case = Case("c2")
+    runs = []
+    for _ in range(3):
+        eng = case.engine(STEPS, pool_dtype="f16", cuda_graph=graph)
+        try:
+            outs = []
+            for _ in range(STEPS):
+                outs.append(eng.decode_step().cpu().numpy().copy())
+            torch.cuda.synchronize()
+            runs.append((np.stack(outs), eng.n.cpu().numpy().copy(), eng.idx.cpu().numpy().copy()))
+        finally:
+            eng.close()
+            del eng
+            torch.cuda.empty_cache()
+    for r in runs[1:]:
+        np.testing.assert_array_equal(r[0], runs[0][0])
+        np.testing.assert_array_equal(r[1], runs[0][1])
+        np.testing.assert_array_equal(r[2], runs[0][2])
