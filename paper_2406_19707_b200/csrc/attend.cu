@@ -897,7 +897,9 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
         }();
         static const int seg = [] {
           const char* e = getenv("IG_WP_SEG");
-          return e && atoi(e) == 256 ? 256 : (e && atoi(e) == 64 ? 64 : kWpSegDefault);
+          // (no 64-row option: the partial scratch holds cap / kAttChunk = cap / 128
+          // segments per (b, h), so smaller items would overrun a row's slots)
+          return e && atoi(e) == 256 ? 256 : kWpSegDefault;
         }();
         const int per_sm = ring == 2 ? 3 : 2;
         const int maxseg = (cap + seg - 1) / seg;
@@ -913,7 +915,6 @@ int launch_attend(dim3 grid, cudaStream_t s, const float* q, int ldq, const floa
         (int)grid.y, cap, sqrt_d, max_chunks, partial, tickets, out, ldo);                      \
   } while (0)
         if (ring == 2 && seg == 256) IG_ATT_WP(2, 256);
-        else if (ring == 2 && seg == 64) IG_ATT_WP(2, 64);
         else if (ring == 3 && seg == 256) IG_ATT_WP(3, 256);
         else if (ring == 3) IG_ATT_WP(3, kWpSegDefault);
         else IG_ATT_WP(2, kWpSegDefault);
